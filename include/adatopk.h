@@ -1,0 +1,124 @@
+/*
+ * adatopk.h — C-ABI of the B200-native AdaTopK compressor (sm_100a).
+ *
+ * This is the drop-in boundary for the hot path named in BASELINE.json
+ * `north_star`: the Top-K compressor of FusionLLM's reference
+ * (`geopipe.compressor`, /root/reference/pkg/src/geopipe/compressor.py) and the
+ * per-link adaptive ratio bookkeeping (Eq. 6).  Every entry point below cites
+ * the reference function it replaces.  Plain pointers and sizes only: device
+ * pointers for tensors, `void* stream` is a `cudaStream_t` (NULL = legacy
+ * default stream).  All GPU calls are stream-ordered, never synchronise, and
+ * never allocate; the caller owns every buffer.
+ *
+ * Status codes map 1:1 onto the reference exception classes
+ * (/root/reference/pkg/src/geopipe/errors.py:46-59).
+ */
+#ifndef ADATOPK_H_
+#define ADATOPK_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---- status codes ------------------------------------------------------ */
+#define GP_OK                       0
+#define GP_ERR_INVALID_RATIO        1  /* errors.py:46  InvalidRatio      */
+#define GP_ERR_EMPTY_VECTOR         2  /* errors.py:50  EmptyVector       */
+#define GP_ERR_INDEX_OUT_OF_RANGE   3  /* errors.py:54  IndexOutOfRange   */
+#define GP_ERR_NO_COMMUNICATION     4  /* errors.py:58  NoCommunication   */
+#define GP_ERR_CUDA                 5  /* CUDA launch / runtime error      */
+#define GP_ERR_INVALID_ARGUMENT     6  /* bad dtype, size, alignment, ... */
+
+/* ---- element types ----------------------------------------------------- */
+#define GP_DTYPE_F32   0   /* float32  (reference fp32 path)               */
+#define GP_DTYPE_BF16  1   /* bfloat16 (selection == reference on x.float()) */
+#define GP_DTYPE_F64   2   /* float64  (reference executor's dtype)        */
+
+/* ---- asynchronous device error flags (decompress) ---------------------- */
+#define GP_FLAG_OUT_OF_RANGE  1u   /* some index < 0 or >= d  (compressor.py:99-100) */
+#define GP_FLAG_UNSORTED      2u   /* indices not strictly increasing (fast path invalid) */
+
+/* Wire frame of the reference (compressor.py:39-44): little-endian
+ * {d:u64, k:u64} header, k x i64 indices, k x f32 values. */
+#define GP_FRAME_HEADER_BYTES 16
+static inline size_t gp_frame_bytes(int64_t k) { return (size_t)GP_FRAME_HEADER_BYTES + (size_t)k * 12u; }
+
+/* Library version string. */
+const char* gp_version(void);
+
+/* k = max(1, floor(d / ratio)); GP_ERR_INVALID_RATIO if ratio < 1.
+ * Replaces select_k, compressor.py:73-76 (IEEE double divide, same order). */
+int gp_select_k(int64_t d, double ratio, int64_t* k_out);
+
+/* Bytes on the wire for a compressed length-d vector = 12 * k.
+ * Replaces wire_bytes, compressor.py:106-108. */
+int gp_wire_bytes(int64_t d, double ratio, int64_t* bytes_out);
+
+/* Scratch needed by gp_topk_compress for vectors of up to d elements on the
+ * current device.  The workspace must be zeroed once (gp_workspace_init) and is
+ * left zeroed by every successful call; one workspace per concurrent stream. */
+size_t gp_topk_workspace_bytes(int64_t d, int dtype);
+int gp_workspace_init(void* ws, size_t ws_bytes, void* stream);
+
+/* Top-K by |x| with lower-index tie break; NaN ranks below every number.
+ * Writes k indices (strictly increasing; int64 if idx_bytes == 8 else int32)
+ * and k values (val_dtype: GP_DTYPE_F32 or the input dtype).  val2_out, if
+ * non-NULL, receives the values again in the input dtype (lets the caller get
+ * both the f32 wire values and the dtype-preserving SparsePayload.values in one
+ * pass).  header_out, if non-NULL, receives the {d, k} frame header.
+ * Replaces topk_compress, compressor.py:79-94 (np.argsort(-|x|, stable), take
+ * k, sort kept, gather).  d must be < 2^31. */
+int gp_topk_compress(const void* x, int dtype, int64_t d, int64_t k,
+                     void* idx_out, int idx_bytes,
+                     void* val_out, int val_dtype,
+                     void* val2_out,
+                     void* header_out,
+                     void* ws, size_t ws_bytes, void* stream);
+
+/* Same, writing the reference wire frame (16 + 12k bytes) directly. */
+int gp_topk_compress_frame(const void* x, int dtype, int64_t d, int64_t k,
+                           void* frame_out, void* ws, size_t ws_bytes, void* stream);
+
+/* Dense length-d output: values at their indices, zero (mode 0) or added to
+ * the existing contents (mode 1, residual extension) elsewhere.  Fast path,
+ * requires strictly increasing indices; violations and out-of-range indices are
+ * reported asynchronously in *d_err_flag (GP_FLAG_*; the caller zeroes it).
+ * Replaces topk_decompress, compressor.py:97-103. */
+int gp_topk_decompress(const void* idx, int idx_bytes,
+                       const void* vals, int val_dtype, int64_t k, int64_t d,
+                       void* out, int out_dtype, int mode,
+                       uint32_t* d_err_flag, void* stream);
+
+/* Decompress straight from a reference wire frame on the device. */
+int gp_topk_decompress_frame(const void* frame, int64_t k, int64_t d,
+                             void* out, int out_dtype, int mode,
+                             uint32_t* d_err_flag, void* stream);
+
+/* General scatter for arbitrary (unsorted, possibly repeated) indices with
+ * numpy's last-write-wins semantics for `out[indices] = values`.  `scratch`
+ * holds d int32.  Mode 0 only. */
+int gp_topk_decompress_unsorted(const void* idx, int idx_bytes,
+                                const void* vals, int val_dtype, int64_t k, int64_t d,
+                                void* out, int out_dtype, void* scratch,
+                                uint32_t* d_err_flag, void* stream);
+
+/* On-device AdaTopK bookkeeping (Eq. 6): r_i = max(1, 3*r*R_i/max R) in IEEE
+ * double, same operation order as compressor.py:111-129, then
+ * k_i = max(1, floor(d_i / r_i)) (compressor.py:73-76).  R, d_per_link, r_out,
+ * k_out are device arrays of n entries; *d_status receives GP_OK,
+ * GP_ERR_INVALID_RATIO or GP_ERR_NO_COMMUNICATION. */
+int gp_adatopk_plan(const double* R, int n, double base_ratio,
+                    const int64_t* d_per_link, double* r_out, int64_t* k_out,
+                    int32_t* d_status, void* stream);
+
+/* Host twin of gp_adatopk_plan (same arithmetic), returns the status. */
+int gp_adatopk_plan_host(const double* R, int n, double base_ratio,
+                         const int64_t* d_per_link, double* r_out, int64_t* k_out);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* ADATOPK_H_ */

@@ -1,0 +1,62 @@
+"""ctypes binding of libadatopk.so (the C-ABI in include/adatopk.h).
+
+There is no CPU fallback: if the library is missing the import of any compute
+entry point fails loudly.
+"""
+from __future__ import annotations
+
+import ctypes
+from ctypes import c_double, c_int, c_int32, c_int64, c_size_t, c_void_p, POINTER
+from pathlib import Path
+
+LIB_PATH = Path(__file__).resolve().parent / "_lib" / "libadatopk.so"
+
+DTYPE_F32 = 0
+DTYPE_BF16 = 1
+DTYPE_F64 = 2
+FLAG_OUT_OF_RANGE = 1
+FLAG_UNSORTED = 2
+FRAME_HEADER_BYTES = 16
+
+_SIGS = {
+    "gp_version": (ctypes.c_char_p, []),
+    "gp_select_k": (c_int, [c_int64, c_double, POINTER(c_int64)]),
+    "gp_wire_bytes": (c_int, [c_int64, c_double, POINTER(c_int64)]),
+    "gp_topk_workspace_bytes": (c_size_t, [c_int64, c_int]),
+    "gp_workspace_init": (c_int, [c_void_p, c_size_t, c_void_p]),
+    "gp_topk_compress": (c_int, [c_void_p, c_int, c_int64, c_int64, c_void_p, c_int, c_void_p, c_int,
+                                 c_void_p, c_void_p, c_void_p, c_size_t, c_void_p]),
+    "gp_topk_compress_frame": (c_int, [c_void_p, c_int, c_int64, c_int64, c_void_p, c_void_p, c_size_t,
+                                       c_void_p]),
+    "gp_topk_decompress": (c_int, [c_void_p, c_int, c_void_p, c_int, c_int64, c_int64, c_void_p, c_int, c_int,
+                                   c_void_p, c_void_p]),
+    "gp_topk_decompress_frame": (c_int, [c_void_p, c_int64, c_int64, c_void_p, c_int, c_int, c_void_p,
+                                         c_void_p]),
+    "gp_topk_decompress_unsorted": (c_int, [c_void_p, c_int, c_void_p, c_int, c_int64, c_int64, c_void_p, c_int,
+                                            c_void_p, c_void_p, c_void_p]),
+    "gp_adatopk_plan": (c_int, [POINTER(c_double), c_int, c_double, POINTER(c_int64), POINTER(c_double),
+                                POINTER(c_int64), POINTER(c_int32), c_void_p]),
+    "gp_adatopk_plan_host": (c_int, [POINTER(c_double), c_int, c_double, POINTER(c_int64), POINTER(c_double),
+                                     POINTER(c_int64)]),
+}
+
+EXPORTED = tuple(_SIGS)
+
+_lib = None
+
+
+def lib() -> ctypes.CDLL:
+    """Load (once) and return the C-ABI library."""
+    global _lib
+    if _lib is None:
+        if not LIB_PATH.exists():
+            raise ImportError(
+                f"{LIB_PATH} is not built; run `python -c 'import __graft_entry__ as g; g.build()'` "
+                "(the AdaTopK path has no CPU fallback)")
+        handle = ctypes.CDLL(str(LIB_PATH))
+        for name, (res, args) in _SIGS.items():
+            fn = getattr(handle, name)
+            fn.restype = res
+            fn.argtypes = args
+        _lib = handle
+    return _lib

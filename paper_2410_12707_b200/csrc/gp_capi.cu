@@ -1,0 +1,210 @@
+// gp_capi.cu — the extern "C" boundary (include/adatopk.h) and the on-device
+// AdaTopK bookkeeping kernel.
+//
+// Reference interfaces replaced (pkg/src/geopipe/compressor.py):
+//   select_k        :73-76    -> gp_select_k
+//   wire_bytes      :106-108  -> gp_wire_bytes
+//   topk_compress   :79-94    -> gp_topk_compress / gp_topk_compress_frame
+//   topk_decompress :97-103   -> gp_topk_decompress / _frame / _unsorted
+//   adatopk_plan    :111-129  -> gp_adatopk_plan (device) / gp_adatopk_plan_host
+//   SparsePayload.to_bytes :39-44 -> the *_frame variants write/read that layout
+#include <cmath>
+#include <cstdio>
+
+#include "../../include/adatopk.h"
+#include "gp_kernels.cuh"
+
+namespace {
+
+int device_info(gp::DeviceInfo* info) {
+  static int cached_sms[64] = {0};
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return GP_ERR_CUDA;
+  if (!cached_sms[dev]) {
+    int sms = 0;
+    if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || sms < 1)
+      return GP_ERR_CUDA;
+    cached_sms[dev] = sms;
+  }
+  info->ordinal = dev;
+  info->num_sms = cached_sms[dev];
+  return GP_OK;
+}
+
+inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+
+// Python: `max(1, math.floor(d / ratio))` with `ratio < 1 -> InvalidRatio`.
+int select_k_impl(int64_t d, double ratio, int64_t* k_out) {
+  if (ratio < 1.0) return GP_ERR_INVALID_RATIO;
+  if (std::isnan(ratio)) return GP_ERR_INVALID_ARGUMENT;  // math.floor(nan) raises ValueError
+  const double q = (double)d / ratio;
+  const double f = std::floor(q);
+  int64_t k = (int64_t)f;
+  if (k < 1) k = 1;
+  *k_out = k;
+  return GP_OK;
+}
+
+// Eq. 6 (compressor.py:118-125), operation order preserved:
+//   r_max = max(R); r_i = max(1.0, 3.0 * base_ratio * R_i / r_max)
+__host__ __device__ inline int plan_impl(const double* R, int n, double base, const int64_t* dl, double* r_out,
+                                         int64_t* k_out) {
+  if (base < 1.0) return GP_ERR_INVALID_RATIO;
+  double r_max = 0.0;  // max(values, default=0.0): first element, then strictly-greater updates
+  for (int i = 0; i < n; ++i)
+    if (i == 0 || R[i] > r_max) r_max = R[i];
+  if (r_max <= 0.0) return GP_ERR_NO_COMMUNICATION;
+  for (int i = 0; i < n; ++i) {
+    double t = 3.0 * base;
+    t = t * R[i];
+    t = t / r_max;
+    const double r = (t > 1.0) ? t : 1.0;  // max(1.0, t)
+    if (r_out) r_out[i] = r;
+    if (k_out && dl) {
+      double f = floor((double)dl[i] / r);
+      int64_t k = (int64_t)f;
+      k_out[i] = k < 1 ? 1 : k;
+    }
+  }
+  return GP_OK;
+}
+
+__global__ void plan_kernel(const double* R, int n, double base, const int64_t* dl, double* r_out, int64_t* k_out,
+                            int32_t* status) {
+  if (blockIdx.x == 0 && threadIdx.x == 0) *status = plan_impl(R, n, base, dl, r_out, k_out);
+}
+
+}  // namespace
+
+namespace gp {
+int launch_adatopk_plan(const double* R, int n, double base, const int64_t* dl, double* r_out, int64_t* k_out,
+                        int32_t* status, cudaStream_t s) {
+  plan_kernel<<<1, 32, 0, s>>>(R, n, base, dl, r_out, k_out, status);
+  return cudaGetLastError() == cudaSuccess ? GP_OK : GP_ERR_CUDA;
+}
+}  // namespace gp
+
+extern "C" {
+
+const char* gp_version(void) { return "adatopk-b200 0.1.0 sm_100a"; }
+
+int gp_select_k(int64_t d, double ratio, int64_t* k_out) {
+  if (!k_out) return GP_ERR_INVALID_ARGUMENT;
+  return select_k_impl(d, ratio, k_out);
+}
+
+int gp_wire_bytes(int64_t d, double ratio, int64_t* bytes_out) {
+  if (!bytes_out) return GP_ERR_INVALID_ARGUMENT;
+  int64_t k = 0;
+  const int st = select_k_impl(d, ratio, &k);
+  if (st) return st;
+  *bytes_out = k * 12;
+  return GP_OK;
+}
+
+size_t gp_topk_workspace_bytes(int64_t d, int dtype) {
+  if (d < 0) d = 0;
+  return gp::compress_workspace_layout((uint64_t)d, dtype, gp::kMaxGrid, nullptr);
+}
+
+int gp_workspace_init(void* ws, size_t ws_bytes, void* stream) {
+  if (!ws) return GP_ERR_INVALID_ARGUMENT;
+  gp::WsLayout l;
+  gp::compress_workspace_layout(0, 0, gp::kMaxGrid, &l);
+  const size_t n = ws_bytes < l.lists ? ws_bytes : l.lists;  // only state that must start zeroed
+  return cudaMemsetAsync(ws, 0, n, as_stream(stream)) == cudaSuccess ? GP_OK : GP_ERR_CUDA;
+}
+
+int gp_topk_compress(const void* x, int dtype, int64_t d, int64_t k, void* idx_out, int idx_bytes, void* val_out,
+                     int val_dtype, void* val2_out, void* header_out, void* ws, size_t ws_bytes, void* stream) {
+  if (d <= 0) return GP_ERR_EMPTY_VECTOR;
+  if (!x || !idx_out || !val_out || !ws) return GP_ERR_INVALID_ARGUMENT;
+  if (dtype < 0 || dtype > 2) return GP_ERR_INVALID_ARGUMENT;
+  if (d >= (int64_t)1 << 31 || k < 1 || k > d) return GP_ERR_INVALID_ARGUMENT;
+  if (idx_bytes != 4 && idx_bytes != 8) return GP_ERR_INVALID_ARGUMENT;
+  if (val_dtype != GP_DTYPE_F32 && val_dtype != dtype) return GP_ERR_INVALID_ARGUMENT;
+  gp::WsLayout l;
+  const size_t need = gp::compress_workspace_layout((uint64_t)d, dtype, gp::kMaxGrid, &l);
+  if (ws_bytes < need) return GP_ERR_INVALID_ARGUMENT;
+  gp::DeviceInfo dev;
+  if (device_info(&dev)) return GP_ERR_CUDA;
+  unsigned char* base = static_cast<unsigned char*>(ws);
+  gp::CompressArgs a = {};
+  a.x = x;
+  a.d = (uint32_t)d;
+  a.k = (uint32_t)k;
+  a.idx_out = idx_out;
+  a.idx64 = idx_bytes == 8;
+  a.val_out = val_out;
+  a.val_f32 = val_dtype == GP_DTYPE_F32;
+  a.val2_out = val2_out;
+  a.header = static_cast<unsigned long long*>(header_out);
+  a.ctrl = reinterpret_cast<uint32_t*>(base + l.ctrl);
+  a.hist1 = reinterpret_cast<uint32_t*>(base + l.hist1);
+  a.hist_lvl = reinterpret_cast<uint32_t*>(base + l.hist_lvl);
+  a.cta_a = reinterpret_cast<uint32_t*>(base + l.cta_a);
+  a.cta_b = reinterpret_cast<uint32_t*>(base + l.cta_b);
+  a.fcreg = base + l.fcreg;
+  a.lists = base + l.lists;
+  a.aligned = ((uintptr_t)x % 16) == 0;
+  return gp::launch_compress(dtype, a, dev, as_stream(stream));
+}
+
+int gp_topk_compress_frame(const void* x, int dtype, int64_t d, int64_t k, void* frame_out, void* ws,
+                           size_t ws_bytes, void* stream) {
+  if (!frame_out || ((uintptr_t)frame_out % 8) != 0) return GP_ERR_INVALID_ARGUMENT;
+  unsigned char* f = static_cast<unsigned char*>(frame_out);
+  return gp_topk_compress(x, dtype, d, k, f + GP_FRAME_HEADER_BYTES, 8, f + GP_FRAME_HEADER_BYTES + 8 * k,
+                          GP_DTYPE_F32, nullptr, f, ws, ws_bytes, stream);
+}
+
+static int decompress_common(const void* idx, int idx_bytes, const void* vals, int val_dtype, int64_t k, int64_t d,
+                             void* out, int out_dtype, int mode, uint32_t* d_err_flag, void* stream,
+                             void* scratch) {
+  if (k < 0 || d < 0) return GP_ERR_INVALID_ARGUMENT;
+  if (idx_bytes != 4 && idx_bytes != 8) return GP_ERR_INVALID_ARGUMENT;
+  if (val_dtype < 0 || val_dtype > 2 || out_dtype < 0 || out_dtype > 2) return GP_ERR_INVALID_ARGUMENT;
+  if (mode != 0 && mode != 1) return GP_ERR_INVALID_ARGUMENT;
+  if (!d_err_flag || (k > 0 && (!idx || !vals)) || (d > 0 && !out)) return GP_ERR_INVALID_ARGUMENT;
+  if (d == 0 && k > 0) return GP_ERR_INDEX_OUT_OF_RANGE;  // every index is >= d
+  gp::DeviceInfo dev;
+  if (device_info(&dev)) return GP_ERR_CUDA;
+  gp::DecompressArgs a = {idx, idx_bytes == 8, vals, val_dtype, k, d, out, out_dtype, mode, d_err_flag};
+  if (scratch) return gp::launch_decompress_unsorted(a, scratch, dev, as_stream(stream));
+  return gp::launch_decompress(a, dev, as_stream(stream));
+}
+
+int gp_topk_decompress(const void* idx, int idx_bytes, const void* vals, int val_dtype, int64_t k, int64_t d,
+                       void* out, int out_dtype, int mode, uint32_t* d_err_flag, void* stream) {
+  return decompress_common(idx, idx_bytes, vals, val_dtype, k, d, out, out_dtype, mode, d_err_flag, stream, nullptr);
+}
+
+int gp_topk_decompress_frame(const void* frame, int64_t k, int64_t d, void* out, int out_dtype, int mode,
+                             uint32_t* d_err_flag, void* stream) {
+  if (!frame || ((uintptr_t)frame % 8) != 0) return GP_ERR_INVALID_ARGUMENT;
+  const unsigned char* f = static_cast<const unsigned char*>(frame);
+  return decompress_common(f + GP_FRAME_HEADER_BYTES, 8, f + GP_FRAME_HEADER_BYTES + 8 * k, GP_DTYPE_F32, k, d, out,
+                           out_dtype, mode, d_err_flag, stream, nullptr);
+}
+
+int gp_topk_decompress_unsorted(const void* idx, int idx_bytes, const void* vals, int val_dtype, int64_t k,
+                                int64_t d, void* out, int out_dtype, void* scratch, uint32_t* d_err_flag,
+                                void* stream) {
+  if (!scratch) return GP_ERR_INVALID_ARGUMENT;
+  if (d >= (int64_t)1 << 31 || k >= (int64_t)1 << 31) return GP_ERR_INVALID_ARGUMENT;
+  return decompress_common(idx, idx_bytes, vals, val_dtype, k, d, out, out_dtype, 0, d_err_flag, stream, scratch);
+}
+
+int gp_adatopk_plan(const double* R, int n, double base_ratio, const int64_t* d_per_link, double* r_out,
+                    int64_t* k_out, int32_t* d_status, void* stream) {
+  if (!R || !d_status || n < 0) return GP_ERR_INVALID_ARGUMENT;
+  return gp::launch_adatopk_plan(R, n, base_ratio, d_per_link, r_out, k_out, d_status, as_stream(stream));
+}
+
+int gp_adatopk_plan_host(const double* R, int n, double base_ratio, const int64_t* d_per_link, double* r_out,
+                         int64_t* k_out) {
+  if ((!R && n > 0) || n < 0) return GP_ERR_INVALID_ARGUMENT;
+  return plan_impl(R, n, base_ratio, d_per_link, r_out, k_out);
+}
+
+}  // extern "C"

@@ -1,0 +1,218 @@
+// gp_decompress.cu — AdaTopK decompress on sm_100a.
+//
+// Replaces topk_decompress (reference: pkg/src/geopipe/compressor.py:97-103):
+//     if k and (indices.min() < 0 or indices.max() >= d): raise IndexOutOfRange
+//     out = np.zeros(d, values.dtype); out[indices] = values
+//
+// Fast path (indices strictly increasing, as topk_compress emits them): one
+// CTA per 4096-element output tile.  Two warps locate the tile's slice of the
+// index array with a 32-ary search, the tile is zero-filled (or, mode 1, loaded
+// for a residual add) in shared memory, the slice is scattered into it, and the
+// tile is written to HBM once with 128-bit stores — every output element is
+// written exactly once.  The same launch validates the index array: each CTA
+// checks a 1/grid share of the k-1 adjacent pairs (strictly increasing) and
+// CTA 0 checks idx[0] >= 0 and idx[k-1] < d; violations are reported in an
+// asynchronous device flag (GP_FLAG_*).
+//
+// General path (unsorted / repeated indices) reproduces numpy's
+// last-write-wins `out[indices] = values` with an atomicMax "winner" pass.
+#include <type_traits>
+
+#include "gp_kernels.cuh"
+
+namespace gp {
+
+constexpr int kTile = 4096;
+constexpr int kDecThreads = 256;
+
+// ---- value conversions (exact for f32<->f64 widening and bf16<->f32 of bf16 values)
+__device__ __forceinline__ float bf16_to_f32(uint16_t b) { return __uint_as_float((uint32_t)b << 16); }
+__device__ __forceinline__ uint16_t f32_to_bf16_rn(float f) {
+  uint32_t u = __float_as_uint(f);
+  if ((u & 0x7FFFFFFFu) > 0x7F800000u) return (uint16_t)((u >> 16) | 0x40u);
+  u += 0x7FFFu + ((u >> 16) & 1u);
+  return (uint16_t)(u >> 16);
+}
+
+template <class T> struct Val;
+template <> struct Val<float> {
+  __device__ static double to_d(float v) { return (double)v; }
+  __device__ static float to_f(float v) { return v; }
+};
+template <> struct Val<uint16_t> {
+  __device__ static double to_d(uint16_t v) { return (double)bf16_to_f32(v); }
+  __device__ static float to_f(uint16_t v) { return bf16_to_f32(v); }
+};
+template <> struct Val<double> {
+  __device__ static double to_d(double v) { return v; }
+  __device__ static float to_f(double v) { return __double2float_rn(v); }
+};
+
+template <class O, class V>
+__device__ __forceinline__ O cvt(V v) {
+  if constexpr (std::is_same<O, V>::value) return v;
+  else if constexpr (std::is_same<O, double>::value) return Val<V>::to_d(v);
+  else if constexpr (std::is_same<O, float>::value) return Val<V>::to_f(v);
+  else return f32_to_bf16_rn(Val<V>::to_f(v));
+}
+
+template <class O>
+__device__ __forceinline__ O add_vals(O a, O b) {
+  if constexpr (std::is_same<O, uint16_t>::value) return f32_to_bf16_rn(bf16_to_f32(a) + bf16_to_f32(b));
+  else return a + b;
+}
+
+// first j in [0, n) with idx[j] >= target (n if none), computed by one warp.
+template <class IT>
+__device__ __forceinline__ int64_t warp_lower_bound(const IT* __restrict__ idx, int64_t n, int64_t target) {
+  const uint32_t lane = threadIdx.x & 31;
+  int64_t lo = 0, hi = n;
+  while (hi - lo > 32) {
+    const int64_t span = hi - lo;
+    const int64_t p = lo + (span * (lane + 1)) / 33;
+    const bool pred = (int64_t)__ldg(idx + p) < target;
+    const int cnt = __popc(__ballot_sync(kFull, pred));
+    const int64_t nlo = cnt > 0 ? lo + (span * cnt) / 33 + 1 : lo;
+    const int64_t nhi = cnt < 32 ? lo + (span * (cnt + 1)) / 33 : hi;
+    lo = nlo;
+    hi = nhi;
+  }
+  const int64_t p = lo + lane;
+  const bool pred = p < hi && (int64_t)__ldg(idx + p) < target;
+  return lo + __popc(__ballot_sync(kFull, pred));
+}
+
+template <class IT, class VT, class OT>
+__global__ void __launch_bounds__(kDecThreads) decompress_kernel(const IT* __restrict__ idx,
+                                                                 const VT* __restrict__ vals, int64_t k,
+                                                                 int64_t d, OT* __restrict__ out, int mode,
+                                                                 uint32_t* err, int aligned) {
+  __shared__ __align__(16) OT tile[kTile];
+  __shared__ int64_t sh_range[2];
+  const uint32_t tid = threadIdx.x, w = tid >> 5, lane = tid & 31;
+  const int64_t t0 = (int64_t)blockIdx.x * kTile;
+  const int64_t t1 = min(t0 + (int64_t)kTile, d);
+  const int n = (int)(t1 - t0);
+  const bool full = aligned && n == kTile;
+
+  if (w < 2) {
+    const int64_t r = warp_lower_bound(idx, k, w == 0 ? t0 : t1);
+    if (lane == 0) sh_range[w] = r;
+  }
+  constexpr int kVecs = kTile * (int)sizeof(OT) / 16;
+  uint4* tv = reinterpret_cast<uint4*>(tile);
+  if (mode == 0) {
+    for (int i = tid; i < kVecs; i += kDecThreads) tv[i] = make_uint4(0u, 0u, 0u, 0u);
+  } else if (full) {
+    const uint4* ov = reinterpret_cast<const uint4*>(out + t0);
+    for (int i = tid; i < kVecs; i += kDecThreads) tv[i] = ov[i];
+  } else {
+    for (int i = tid; i < n; i += kDecThreads) tile[i] = out[t0 + i];
+  }
+  __syncthreads();
+  const int64_t lo = sh_range[0], hi = sh_range[1];
+  bool bad = false;
+  for (int64_t j = lo + tid; j < hi; j += kDecThreads) {
+    const int64_t i = (int64_t)idx[j];
+    if (i >= t0 && i < t1) {
+      const OT v = cvt<OT>(vals[j]);
+      tile[i - t0] = mode == 0 ? v : add_vals<OT>(tile[i - t0], v);
+    } else {
+      bad = true;
+    }
+  }
+  // validation share: pairs [pb, pe) must be strictly increasing
+  if (k > 1) {
+    const int64_t P = k - 1;
+    const int64_t pb = (P * (int64_t)blockIdx.x) / gridDim.x;
+    const int64_t pe = (P * ((int64_t)blockIdx.x + 1)) / gridDim.x;
+    for (int64_t j = pb + tid; j < pe; j += kDecThreads)
+      if (!((int64_t)idx[j] < (int64_t)idx[j + 1])) bad = true;
+  }
+  if (__syncthreads_or(bad) && tid == 0) atomicOr(err, 2u);
+  if (blockIdx.x == 0 && tid == 0 && k > 0) {
+    if ((int64_t)idx[0] < 0 || (int64_t)idx[k - 1] >= d) atomicOr(err, 1u);
+  }
+  if (full) {
+    uint4* ov = reinterpret_cast<uint4*>(out + t0);
+    for (int i = tid; i < kVecs; i += kDecThreads) ov[i] = tv[i];
+  } else {
+    for (int i = tid; i < n; i += kDecThreads) out[t0 + i] = tile[i];
+  }
+}
+
+// ---- general path
+template <class OT>
+__global__ void zero_kernel(OT* out, int64_t d) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < d; i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = OT(0);
+}
+
+template <class IT>
+__global__ void winner_kernel(const IT* idx, int64_t k, int64_t d, int32_t* win, uint32_t* err) {
+  for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < k; j += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = (int64_t)idx[j];
+    if (i < 0 || i >= d) atomicOr(err, 1u);
+    else atomicMax(&win[i], (int32_t)j);
+  }
+}
+
+template <class IT, class VT, class OT>
+__global__ void scatter_kernel(const IT* idx, const VT* vals, int64_t k, int64_t d, const int32_t* win, OT* out) {
+  for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < k; j += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = (int64_t)idx[j];
+    if (i >= 0 && i < d && win[i] == (int32_t)j) out[i] = cvt<OT>(vals[j]);
+  }
+}
+
+// ---- dispatch
+template <class IT, class VT, class OT>
+static int run_fast(const DecompressArgs& a, cudaStream_t s) {
+  if (a.d <= 0) return 0;
+  const int64_t tiles = (a.d + kTile - 1) / kTile;
+  const int aligned = ((uintptr_t)a.out % 16) == 0;
+  decompress_kernel<IT, VT, OT><<<(unsigned)tiles, kDecThreads, 0, s>>>(
+      (const IT*)a.idx, (const VT*)a.vals, a.k, a.d, (OT*)a.out, a.mode, a.err, aligned);
+  return cudaGetLastError() == cudaSuccess ? 0 : 5;
+}
+
+template <class IT, class VT, class OT>
+static int run_general(const DecompressArgs& a, void* scratch, const DeviceInfo& dev, cudaStream_t s) {
+  const unsigned blocks = (unsigned)dev.num_sms * 8;
+  zero_kernel<OT><<<blocks, 256, 0, s>>>((OT*)a.out, a.d);
+  if (cudaMemsetAsync(scratch, 0xFF, (size_t)a.d * 4, s) != cudaSuccess) return 5;
+  winner_kernel<IT><<<blocks, 256, 0, s>>>((const IT*)a.idx, a.k, a.d, (int32_t*)scratch, a.err);
+  scatter_kernel<IT, VT, OT><<<blocks, 256, 0, s>>>((const IT*)a.idx, (const VT*)a.vals, a.k, a.d,
+                                                    (const int32_t*)scratch, (OT*)a.out);
+  return cudaGetLastError() == cudaSuccess ? 0 : 5;
+}
+
+template <class IT, class VT>
+static int pick_out(const DecompressArgs& a, void* scratch, const DeviceInfo& dev, cudaStream_t s, bool general) {
+  switch (a.out_dtype) {
+    case 0: return general ? run_general<IT, VT, float>(a, scratch, dev, s) : run_fast<IT, VT, float>(a, s);
+    case 1: return general ? run_general<IT, VT, uint16_t>(a, scratch, dev, s) : run_fast<IT, VT, uint16_t>(a, s);
+    case 2: return general ? run_general<IT, VT, double>(a, scratch, dev, s) : run_fast<IT, VT, double>(a, s);
+    default: return 6;
+  }
+}
+
+template <class IT>
+static int pick_val(const DecompressArgs& a, void* scratch, const DeviceInfo& dev, cudaStream_t s, bool general) {
+  switch (a.val_dtype) {
+    case 0: return pick_out<IT, float>(a, scratch, dev, s, general);
+    case 1: return pick_out<IT, uint16_t>(a, scratch, dev, s, general);
+    case 2: return pick_out<IT, double>(a, scratch, dev, s, general);
+    default: return 6;
+  }
+}
+
+int launch_decompress(const DecompressArgs& a, const DeviceInfo& dev, cudaStream_t s) {
+  return a.idx64 ? pick_val<int64_t>(a, nullptr, dev, s, false) : pick_val<int32_t>(a, nullptr, dev, s, false);
+}
+
+int launch_decompress_unsorted(const DecompressArgs& a, void* scratch, const DeviceInfo& dev, cudaStream_t s) {
+  return a.idx64 ? pick_val<int64_t>(a, scratch, dev, s, true) : pick_val<int32_t>(a, scratch, dev, s, true);
+}
+
+}  // namespace gp

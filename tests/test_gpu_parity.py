@@ -1,0 +1,398 @@
+"""GPU parity of the sm_100a kernels against the reference (golden frames) and the oracle.
+
+Bar: bit-exact.  Compressed frames must equal the reference's
+SparsePayload.to_bytes() byte-for-byte; decompressed tensors must equal the
+reference's topk_decompress bit-for-bit.
+"""
+import ctypes
+import itertools
+
+import numpy as np
+import pytest
+import torch
+from hypothesis import given, settings, strategies as st
+
+import paper_2410_12707_b200 as P
+from paper_2410_12707_b200 import _lib
+from golden_cases import cases, plans
+from oracle import compressor_oracle as O
+
+pytestmark = pytest.mark.gpu
+
+
+def _bits(t: torch.Tensor) -> np.ndarray:
+    a = t.detach().cpu()
+    if a.dtype == torch.bfloat16:
+        return a.view(torch.int16).numpy().view(np.uint16)
+    return a.numpy().view({4: np.uint32, 8: np.uint64}[a.element_size()])
+
+
+def _bf16_tensor(bits: np.ndarray, device) -> torch.Tensor:
+    return torch.from_numpy(bits.view(np.int16).copy()).view(torch.bfloat16).to(device)
+
+
+# --------------------------------------------------------------------------- golden frames
+
+
+@pytest.mark.parametrize("prefix", ["f32", "f64"])
+def test_golden_frames_bit_exact(cuda, prefix):
+    bad = []
+    for name, x, ratio, frame in cases(prefix):
+        p = P.topk_compress(torch.from_numpy(x.copy()).to(cuda), ratio)
+        if p.to_bytes() != frame:
+            bad.append(name)
+    assert not bad, f"{len(bad)} frames differ, e.g. {bad[:10]}"
+
+
+def test_golden_frames_bf16(cuda):
+    for name, bits, ratio, frame in cases("bf16"):
+        x = _bf16_tensor(bits, cuda)
+        p = P.topk_compress(x, ratio)
+        assert p.to_bytes() == frame, name
+        assert p.values.dtype == torch.bfloat16
+        # values (dtype preserved) agree with the frame's f32 values exactly
+        _, idx, d = O.from_bytes(frame)
+        np.testing.assert_array_equal(_bits(p.values), bits[idx])
+
+
+def test_golden_decompress_bit_exact(cuda):
+    for name, x, ratio, frame in itertools.islice(cases("f32"), 0, None, 7):
+        p = P.topk_compress(torch.from_numpy(x.copy()).to(cuda), ratio)
+        dense = P.topk_decompress(p)
+        vals, idx, d = O.topk_compress(x, ratio)
+        ref = O.topk_decompress(vals, idx, d)
+        assert dense.dtype == torch.float32
+        np.testing.assert_array_equal(_bits(dense), ref.view(np.uint32), err_msg=name)
+
+
+def test_from_bytes_round_trip(cuda):
+    for name, x, ratio, frame in itertools.islice(cases("f32"), 0, None, 13):
+        q = P.SparsePayload.from_bytes(frame, device=cuda)
+        assert q.values.dtype == torch.float64 and q.to_bytes() == frame
+        dense = P.topk_decompress(q)
+        vals, idx, d = O.from_bytes(frame)
+        np.testing.assert_array_equal(dense.cpu().numpy(), O.topk_decompress(vals, idx, d), err_msg=name)
+
+
+# --------------------------------------------------------------------------- reference unit tests, on the GPU
+
+
+class TestReferenceUnitTests:
+    """The reference's tests/test_compressor.py:33-118, run against the GPU path."""
+
+    def test_two_largest(self, cuda):
+        p = P.topk_compress([0.1, -5.0, 3.0, 0.0], 2)
+        assert p.indices.tolist() == [1, 2]
+        assert p.values.tolist() == [-5.0, 3.0]
+
+    def test_ratio_one_identity(self, cuda):
+        v = [1.0, -2.0, 0.5]
+        p = P.topk_compress(v, 1)
+        assert p.k == 3
+        assert P.topk_decompress(p).tolist() == v
+
+    def test_magnitude_tie_lower_index(self, cuda):
+        p = P.topk_compress([2.0, -2.0, 1.0], 3)
+        assert p.indices.tolist() == [0] and p.values.tolist() == [2.0]
+
+    def test_empty_vector(self, cuda):
+        with pytest.raises(P.EmptyVector):
+            P.topk_compress([], 2)
+        with pytest.raises(P.EmptyVector):
+            P.topk_compress(torch.empty(0, device=cuda), 2)
+
+    def test_dtype_preserved(self, cuda):
+        p = P.topk_compress(np.array([1.0, 2.0], dtype=np.float64), 2)
+        assert p.values.dtype == torch.float64
+
+    @settings(max_examples=200, deadline=None)
+    @given(st.lists(st.floats(-100, 100), min_size=1, max_size=12), st.floats(1, 20))
+    def test_matches_brute_force(self, cuda, values, ratio):
+        p = P.topk_compress(values, ratio)
+        k = P.select_k(len(values), ratio)
+        best = None
+        for combo in itertools.combinations(range(len(values)), k):
+            score = tuple(sorted((abs(values[i]) for i in combo), reverse=True))
+            if best is None or score > best[0]:
+                best = (score, combo)
+        assert set(p.indices.tolist()) == set(best[1])
+
+    @settings(max_examples=50, deadline=None)
+    @given(st.lists(st.floats(-100, 100), min_size=2, max_size=30))
+    def test_error_monotone_in_kept_count(self, cuda, values):
+        v = torch.tensor(values, dtype=torch.float64, device=cuda)
+        errs = []
+        for ratio in (8, 4, 2, 1):
+            rec = P.topk_decompress(P.topk_compress(v, ratio))
+            errs.append(float(torch.linalg.norm(v - rec)))
+        assert all(a >= b - 1e-12 for a, b in zip(errs, errs[1:]))
+
+    def test_inverse_on_support(self, cuda):
+        p = P.topk_compress([0.1, -5.0, 3.0, 0.0], 2)
+        assert P.topk_decompress(p).tolist() == [0.0, -5.0, 3.0, 0.0]
+
+    def test_all_zero_vector(self, cuda):
+        assert P.topk_decompress(P.topk_compress(np.zeros(8), 4)).tolist() == [0.0] * 8
+
+    def test_payload_matches_wire_bytes(self, cuda):
+        rng = np.random.default_rng(1)
+        for d, ratio in [(10, 2), (100, 100), (7, 3.5)]:
+            p = P.topk_compress(rng.standard_normal(d), ratio)
+            assert p.payload_nbytes == P.wire_bytes(d, ratio)
+            assert len(p.to_bytes()) == 16 + P.wire_bytes(d, ratio)
+
+    def test_byte_round_trip(self, cuda):
+        p = P.topk_compress(np.array([1.5, -2.25, 0.125, 4.0], dtype=np.float32), 2)
+        q = P.SparsePayload.from_bytes(p.to_bytes())
+        assert q.original_len == 4 and q.indices.tolist() == p.indices.tolist()
+        assert q.values.tolist() == p.values.tolist()
+
+
+# --------------------------------------------------------------------------- sizes of the BASELINE configs
+
+
+def _check_against_oracle(x: torch.Tensor, ratio: float):
+    p = P.topk_compress(x, ratio)
+    xf = x.float() if x.dtype == torch.bfloat16 else x
+    host = xf.cpu().numpy()
+    vals, idx, d = O.topk_compress(host, ratio, method="threshold")
+    got_idx = p.indices.cpu().numpy()
+    np.testing.assert_array_equal(got_idx, idx)
+    assert p.to_bytes() == O.to_bytes(vals, idx, d)
+    return p
+
+
+@pytest.mark.parametrize("ratio", [10, 100, 1000, 10000])
+def test_c1_gpt2_small_activation(cuda, ratio):
+    """configs[0]: 8x1024x768 fp32 (d = 6,291,456)."""
+    g = torch.Generator(device=cuda).manual_seed(0)
+    x = torch.randn(8, 1024, 768, device=cuda, generator=g)
+    p = _check_against_oracle(x, ratio)
+    dense = P.topk_decompress(p)
+    ref = torch.zeros_like(x.reshape(-1))
+    ref[p.indices] = x.reshape(-1)[p.indices]
+    assert torch.equal(dense.view(torch.int32), ref.view(torch.int32))
+
+
+@pytest.mark.parametrize("dist", ["relu", "laplace", "student_t", "outlier_channels", "quantized"])
+def test_c1_variants(cuda, dist):
+    g = torch.Generator(device=cuda).manual_seed(1)
+    x = torch.randn(8, 1024, 768, device=cuda, generator=g)
+    if dist == "relu":
+        x = torch.relu(x)
+        ratios = (1.5, 10, 100)
+    elif dist == "laplace":
+        x = torch.sign(x) * torch.log1p(x.abs() * 10)
+        ratios = (100,)
+    elif dist == "student_t":
+        x = x / torch.sqrt((torch.randn(x.shape, device=cuda, generator=g) ** 2 +
+                            torch.randn(x.shape, device=cuda, generator=g) ** 2 +
+                            torch.randn(x.shape, device=cuda, generator=g) ** 2) / 3)
+        ratios = (10, 1000)
+    elif dist == "outlier_channels":
+        x[..., ::97] *= 50.0  # GPT-2 style massive-activation channels
+        ratios = (100, 1000)
+    else:
+        x = torch.round(x * 2) / 2
+        ratios = (10, 100)
+    for r in ratios:
+        _check_against_oracle(x.contiguous(), r)
+
+
+@pytest.mark.parametrize("shape", [(64, 2048, 7, 7), (64, 1024, 14, 14), (64, 512, 28, 28)])
+def test_resnet101_boundaries_vs_oracle(cuda, shape):
+    g = torch.Generator(device=cuda).manual_seed(2)
+    act = torch.relu(torch.randn(shape, device=cuda, generator=g))
+    grad = torch.randn(shape, device=cuda, generator=g) * 1e-3
+    for r in (10, 100, 1000):
+        _check_against_oracle(act, r)
+        _check_against_oracle(grad, r)
+
+
+def test_resnet101_largest_boundary_properties(cuda):
+    """[64,256,56,56] (d = 51,380,224): size-independent properties, no CPU sort."""
+    g = torch.Generator(device=cuda).manual_seed(3)
+    x = torch.relu(torch.randn(64, 256, 56, 56, device=cuda, generator=g)).reshape(-1)
+    for r in (10, 100, 1000):
+        p = P.topk_compress(x, r)
+        k = P.select_k(x.numel(), r)
+        idx = p.indices
+        assert idx.numel() == k
+        assert bool((idx[1:] > idx[:-1]).all())
+        assert torch.equal(p.values, x[idx])
+        kept = torch.zeros(x.numel(), dtype=torch.bool, device=cuda)
+        kept[idx] = True
+        a = x.abs()
+        t_min = a[kept].min()
+        assert bool((a[~kept] <= t_min).all())
+        # ties at the threshold: every dropped element equal to the threshold lies after every kept one
+        eq_dropped = torch.nonzero((~kept) & (a == t_min)).reshape(-1)
+        eq_kept = torch.nonzero(kept & (a == t_min)).reshape(-1)
+        if eq_dropped.numel() and eq_kept.numel():
+            assert int(eq_dropped.min()) > int(eq_kept.max())
+        dense = P.topk_decompress(p)
+        assert torch.equal(dense[idx], x[idx]) and int(torch.count_nonzero(dense[~kept])) == 0
+
+
+def test_bf16_large_vs_oracle(cuda):
+    g = torch.Generator(device=cuda).manual_seed(4)
+    x = torch.randn(8, 1024, 1024, device=cuda, generator=g).to(torch.bfloat16)
+    for r in (10, 100):
+        p = _check_against_oracle(x, r)
+        assert torch.equal(p.values, x.reshape(-1)[p.indices])
+        dense = P.topk_decompress(p)
+        assert dense.dtype == torch.bfloat16
+
+
+def test_f64_vs_oracle(cuda):
+    g = torch.Generator(device=cuda).manual_seed(5)
+    x = torch.randn(300_001, device=cuda, generator=g, dtype=torch.float64)
+    for r in (3, 100):
+        _check_against_oracle(x, r)
+
+
+@pytest.mark.parametrize("d", [1, 2, 3, 7, 8, 9, 31, 33, 255, 4097, 16385, 100_001, 1_000_003])
+def test_odd_sizes(cuda, d):
+    g = torch.Generator(device=cuda).manual_seed(d)
+    x = torch.randn(d, device=cuda, generator=g)
+    for r in (1, 1.7, 10, 1000):
+        _check_against_oracle(x, r)
+
+
+def test_unaligned_input(cuda):
+    g = torch.Generator(device=cuda).manual_seed(6)
+    base = torch.randn(100_003, device=cuda, generator=g)
+    for off in (1, 2, 3):
+        _check_against_oracle(base[off:], 50)
+
+
+def test_deterministic_repeat(cuda):
+    g = torch.Generator(device=cuda).manual_seed(7)
+    x = torch.randn(4, 1024, 1600, device=cuda, generator=g)
+    frames = {P.topk_compress(x, 300).to_bytes() for _ in range(5)}
+    assert len(frames) == 1
+
+
+def test_workspace_reuse_across_sizes_and_dtypes(cuda):
+    """The workspace is left clean by every call (zeroed once)."""
+    g = torch.Generator(device=cuda).manual_seed(8)
+    xs = [torch.randn(n, device=cuda, generator=g) for n in (1000, 3_000_000, 17, 250_000)]
+    for _ in range(2):
+        for x in xs:
+            _check_against_oracle(x, 37)
+            _check_against_oracle(x.to(torch.bfloat16), 11)
+
+
+def test_side_stream(cuda):
+    s = torch.cuda.Stream()
+    g = torch.Generator(device=cuda).manual_seed(9)
+    x = torch.randn(2_000_000, device=cuda, generator=g)
+    torch.cuda.synchronize()
+    with torch.cuda.stream(s):
+        p = P.topk_compress(x, 100)
+        dense = P.topk_decompress(p)
+    s.synchronize()
+    vals, idx, d = O.topk_compress(x.cpu().numpy(), 100, method="threshold")
+    np.testing.assert_array_equal(p.indices.cpu().numpy(), idx)
+    assert torch.equal(dense.cpu()[idx], x.cpu()[idx])
+
+
+# --------------------------------------------------------------------------- decompress edge cases
+
+
+def test_decompress_out_of_range(cuda):
+    for idx in ([0, 5], [-1, 2], [3]):
+        p = P.SparsePayload(values=torch.ones(len(idx), device=cuda),
+                            indices=torch.tensor(idx, device=cuda, dtype=torch.int64), original_len=3)
+        with pytest.raises(P.IndexOutOfRange):
+            P.topk_decompress(p)
+
+
+def test_decompress_unsorted_and_repeated_last_write_wins(cuda):
+    rng = np.random.default_rng(11)
+    d = 100_000
+    idx = rng.integers(0, d, 20_000)
+    vals = rng.standard_normal(20_000).astype(np.float32)
+    ref = np.zeros(d, np.float32)
+    ref[idx] = vals
+    p = P.SparsePayload(values=torch.from_numpy(vals).to(cuda), indices=torch.from_numpy(idx).to(cuda),
+                        original_len=d)
+    out = P.topk_decompress(p)
+    np.testing.assert_array_equal(out.cpu().numpy(), ref)
+
+
+def test_decompress_accumulate_residual(cuda):
+    g = torch.Generator(device=cuda).manual_seed(12)
+    x = torch.randn(1_000_000, device=cuda, generator=g)
+    base = torch.randn(1_000_000, device=cuda, generator=g)
+    p = P.topk_compress(x, 100)
+    out = base.clone()
+    P.topk_decompress(p, out=out, accumulate=True)
+    ref = base.clone()
+    ref[p.indices] += x[p.indices]
+    assert torch.equal(out, ref)
+
+
+def test_decompress_k_zero_and_int32_indices(cuda):
+    p = P.SparsePayload(values=torch.empty(0, device=cuda), indices=torch.empty(0, dtype=torch.int64, device=cuda),
+                        original_len=10)
+    assert P.topk_decompress(p).tolist() == [0.0] * 10
+    x = torch.randn(50_000, device=cuda)
+    q = P.topk_compress(x, 10)
+    q32 = P.SparsePayload(values=q.values, indices=q.indices.to(torch.int32), original_len=q.original_len)
+    assert torch.equal(P.topk_decompress(q32), P.topk_decompress(q))
+
+
+# --------------------------------------------------------------------------- C-ABI directly
+
+
+def test_cabi_frame_entry_points(cuda):
+    L = _lib.lib()
+    g = torch.Generator(device=cuda).manual_seed(13)
+    x = torch.randn(1_234_567, device=cuda, generator=g)
+    d, r = x.numel(), 77.0
+    k = P.select_k(d, r)
+    frame = torch.empty(16 + 12 * k, dtype=torch.uint8, device=cuda)
+    wsb = L.gp_topk_workspace_bytes(d, _lib.DTYPE_F32)
+    ws = torch.empty(wsb, dtype=torch.uint8, device=cuda)
+    s = torch.cuda.current_stream().cuda_stream
+    assert L.gp_workspace_init(ws.data_ptr(), wsb, s) == 0
+    assert L.gp_topk_compress_frame(x.data_ptr(), _lib.DTYPE_F32, d, k, frame.data_ptr(), ws.data_ptr(), wsb, s) == 0
+    assert frame.cpu().numpy().tobytes() == O.compress_frame(x.cpu().numpy(), r, "threshold")
+    out = torch.empty(d, device=cuda)
+    err = torch.zeros(1, dtype=torch.int32, device=cuda)
+    assert L.gp_topk_decompress_frame(frame.data_ptr(), k, d, out.data_ptr(), _lib.DTYPE_F32, 0, err.data_ptr(), s) == 0
+    assert int(err.item()) == 0
+    vals, idx, _ = O.from_bytes(frame.cpu().numpy().tobytes())
+    np.testing.assert_array_equal(out.cpu().numpy(), O.topk_decompress(vals.astype(np.float32), idx, d))
+    # int32 index output
+    i32 = torch.empty(k, dtype=torch.int32, device=cuda)
+    v32 = torch.empty(k, device=cuda)
+    assert L.gp_topk_compress(x.data_ptr(), 0, d, k, i32.data_ptr(), 4, v32.data_ptr(), 0, None, None,
+                              ws.data_ptr(), wsb, s) == 0
+    np.testing.assert_array_equal(i32.cpu().numpy(), idx)
+    # argument validation
+    assert L.gp_topk_compress(x.data_ptr(), 0, 0, 1, i32.data_ptr(), 4, v32.data_ptr(), 0, None, None,
+                              ws.data_ptr(), wsb, s) == 2
+    assert L.gp_topk_compress(x.data_ptr(), 0, d, d + 1, i32.data_ptr(), 4, v32.data_ptr(), 0, None, None,
+                              ws.data_ptr(), wsb, s) == 6
+
+
+def test_device_plan_matches_reference(cuda):
+    for R, r, expected in plans():
+        Rt = torch.tensor(R, dtype=torch.float64, device=cuda)
+        dl = torch.full((len(R),), 6291456, dtype=torch.int64, device=cuda)
+        rr, kk, stt = P.adatopk_plan_device(Rt, r, dl)
+        assert int(stt.item()) == 0
+        assert rr.cpu().tolist() == expected
+        assert kk.cpu().tolist() == [O.select_k(6291456, e) for e in expected]
+    _, _, stt = P.adatopk_plan_device(torch.zeros(2, dtype=torch.float64, device=cuda), 10,
+                                      torch.ones(2, dtype=torch.int64, device=cuda))
+    assert int(stt.item()) == 4  # NoCommunication
+
+
+def test_host_pinned_input_e2e(cuda):
+    x = torch.randn(3_000_000).pin_memory()
+    p = P.topk_compress(x, 100)
+    vals, idx, d = O.topk_compress(x.numpy(), 100, method="threshold")
+    np.testing.assert_array_equal(p.indices.cpu().numpy(), idx)

@@ -1,0 +1,165 @@
+"""Host-side logic and the C-ABI boundary, without a GPU.
+
+Mirrors the reference's own compressor tests that need no numerics
+(tests/test_compressor.py:95-157 of the reference) against the drop-in module,
+and checks that libadatopk.so loads and exports every symbol include/adatopk.h
+declares.
+"""
+import ctypes
+import math
+import re
+from pathlib import Path
+
+import pytest
+from hypothesis import given, settings, strategies as st
+
+import paper_2410_12707_b200 as P
+from paper_2410_12707_b200 import _lib
+from paper_2410_12707_b200.compressor import CompressionPlan
+from golden_cases import plans
+from oracle import compressor_oracle as O
+
+HEADER = Path(__file__).resolve().parent.parent / "include" / "adatopk.h"
+
+
+def test_library_exports_every_declared_symbol():
+    decl = set(re.findall(r"^\s*(?:int|size_t|const char\*)\s+(gp_\w+)\s*\(", HEADER.read_text(), re.M))
+    assert decl, "no declarations parsed"
+    assert decl == set(_lib.EXPORTED)
+    L = _lib.lib()
+    for name in decl:
+        assert getattr(L, name) is not None
+    assert b"sm_100a" in L.gp_version()
+
+
+def test_c_select_k_matches_reference_rule():
+    L = _lib.lib()
+    k = ctypes.c_int64()
+    for d, r in [(100, 100), (1, 1000), (50, 1), (7, 3.5), (6291456, 100), (6291456, 10000.0), (0, 3),
+                 (10, 1.0000001), (2**31 - 1, 7.3)]:
+        assert L.gp_select_k(d, r, ctypes.byref(k)) == 0
+        assert k.value == O.select_k(d, r) == P.select_k(d, r)
+    assert L.gp_select_k(10, 0.5, ctypes.byref(k)) == 1  # InvalidRatio
+    b = ctypes.c_int64()
+    assert L.gp_wire_bytes(100, 100, ctypes.byref(b)) == 0 and b.value == 12
+
+
+@settings(max_examples=300)
+@given(st.integers(0, 2**40), st.floats(1, 1e7))
+def test_select_k_property(d, r):
+    L = _lib.lib()
+    k = ctypes.c_int64()
+    assert L.gp_select_k(d, r, ctypes.byref(k)) == 0
+    assert k.value == max(1, math.floor(d / r)) == P.select_k(d, r)
+
+
+def test_wire_format_constants():
+    # reference tests/test_compressor.py:95-104
+    assert P.wire_bytes(100, 100) == 12
+    assert (100 * 4) / P.wire_bytes(100, 100) == pytest.approx(33.3, abs=0.05)
+    assert P.wire_bytes(50, 1) == 12 * 50
+    assert P.wire_bytes(1, 1000) == 12
+    assert P.VALUE_BYTES == 4 and P.INDEX_BYTES == 8 and P.SPARSE_EXPANSION == 3.0
+
+
+def test_invalid_ratio():
+    with pytest.raises(P.InvalidRatio):
+        P.select_k(10, 0.5)
+    with pytest.raises(P.InvalidRatio):
+        P.uniform_plan([("a", "b")], 0.9)
+    with pytest.raises(P.InvalidRatio):
+        P.adatopk_plan(None, {"L1": 1.0}, 0.5)
+
+
+class TestAdaTopkPlan:
+    """Reference tests/test_compressor.py:121-157 against the drop-in."""
+
+    def test_direct_formula(self):
+        plan = P.adatopk_plan(None, {"L1": 10.0, "L2": 5.0, "L3": 1.0}, 100)
+        assert plan.per_link == {"L1": 300.0, "L2": 150.0, "L3": 30.0}
+
+    def test_clamping(self):
+        plan = P.adatopk_plan(None, {"L1": 10.0, "L2": 0.01}, 100)
+        assert plan.per_link["L1"] == 300.0
+        assert plan.per_link["L2"] == 1.0
+
+    def test_uniform_when_equal(self):
+        plan = P.adatopk_plan(None, {"a": 2.0, "b": 2.0, "c": 2.0}, 50)
+        assert set(plan.per_link.values()) == {150.0}
+
+    def test_no_communication(self):
+        with pytest.raises(P.NoCommunication):
+            P.adatopk_plan(None, {"L1": 0.0}, 10)
+        with pytest.raises(P.NoCommunication):
+            P.adatopk_plan(None, {}, 10)
+
+    @given(st.dictionaries(st.integers(0, 10), st.floats(1e-6, 1e3), min_size=1, max_size=8), st.floats(1, 1e4))
+    def test_argmax_gets_max_and_monotone(self, R, r):
+        plan = P.adatopk_plan(None, R, r)
+        top = max(R, key=lambda k: R[k])
+        assert plan.per_link[top] == max(plan.per_link.values())
+        assert plan.per_link[top] == pytest.approx(3 * r)
+        for a in R:
+            for b in R:
+                if R[a] <= R[b]:
+                    assert plan.per_link[a] <= plan.per_link[b] + 1e-9
+
+    def test_bitwise_equal_to_reference_outputs(self):
+        for R, r, expected in plans():
+            plan = P.adatopk_plan(None, {i: v for i, v in enumerate(R)}, r)
+            assert [plan.per_link[i] for i in range(len(R))] == expected
+
+    def test_host_twin_emits_k(self):
+        L = _lib.lib()
+        R = [3.0, 1.5, 0.001]
+        d = [6291456, 8388608, 4]
+        Ra = (ctypes.c_double * 3)(*R)
+        da = (ctypes.c_int64 * 3)(*d)
+        ra = (ctypes.c_double * 3)()
+        ka = (ctypes.c_int64 * 3)()
+        assert L.gp_adatopk_plan_host(Ra, 3, 100.0, da, ra, ka) == 0
+        ref = O.adatopk_ratios({i: v for i, v in enumerate(R)}, 100.0)
+        for i in range(3):
+            assert ra[i] == ref[i]
+            assert ka[i] == O.select_k(d[i], ref[i])
+
+    def test_uniform_plan(self):
+        plan = P.uniform_plan([("a", "b"), ("b", "c")], 25)
+        assert set(plan.per_link.values()) == {25.0}
+
+    def test_stage_costs_estimates_and_to_dict(self):
+        class SC:
+            devices = ["p0", "p1"]
+            receive = {"p0": 0.5, "p1": 0.25}
+
+        plan = P.adatopk_plan(SC(), {("p0", "p1"): 2.0, ("p1", "p0"): 1.0}, 10)
+        assert plan.R_estimates["p0"] == 0.5 and plan.R_estimates[("p0", "p1")] == 2.0
+        d = plan.to_dict()  # the reference raises TypeError here (mixed keys); the mirror does not
+        assert d["per_link"]["p0->p1"] == 30.0
+
+
+def test_per_device_ratios_and_ratio_for():
+    plan = CompressionPlan(base_ratio=10, per_link={("a", "b"): 10.0, ("c", "b"): 4.0, ("b", "a"): 2.0})
+    assert plan.ratio_for("a", "b") == 10.0 and plan.ratio_for("x", "y") == 1.0
+    out = P.per_device_ratios(plan, ["a", "b", "c"])
+    assert out == {"a": 2.0, "b": 4.0, "c": 1.0}
+    assert P.per_device_ratios(None, ["a"]) == {"a": 1.0}
+
+
+def test_compute_requires_cuda_without_fallback():
+    import torch
+
+    if torch.cuda.is_available():
+        pytest.skip("has a GPU")
+    with pytest.raises(RuntimeError, match="no CPU fallback"):
+        P.topk_compress([1.0, 2.0], 2)
+
+
+def test_status_mapping():
+    from paper_2410_12707_b200.errors import raise_for_status
+
+    for code, exc in [(1, P.InvalidRatio), (2, P.EmptyVector), (3, P.IndexOutOfRange), (4, P.NoCommunication),
+                      (5, RuntimeError), (6, ValueError)]:
+        with pytest.raises(exc):
+            raise_for_status(code)
+    raise_for_status(0)
