@@ -31,6 +31,8 @@ int device_info(gp::DeviceInfo* info) {
   return GP_OK;
 }
 
+unsigned long long* g_debug_stamps = nullptr;  // development aid, see gp_debug_stamps
+
 inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
 
 // Python: `max(1, math.floor(d / ratio))` with `ratio < 1 -> InvalidRatio`.
@@ -87,6 +89,11 @@ int launch_adatopk_plan(const double* R, int n, double base, const int64_t* dl, 
 extern "C" {
 
 const char* gp_version(void) { return "adatopk-b200 0.1.0 sm_100a"; }
+
+// Development aid (not part of the public header): when non-NULL, every
+// compress launch writes per-CTA stage timestamps (globaltimer ns, clock64)
+// into this device buffer of G*32 u64.
+void gp_debug_stamps(void* dev_buf) { g_debug_stamps = static_cast<unsigned long long*>(dev_buf); }
 
 int gp_select_k(int64_t d, double ratio, int64_t* k_out) {
   if (!k_out) return GP_ERR_INVALID_ARGUMENT;
@@ -146,7 +153,8 @@ int gp_topk_compress(const void* x, int dtype, int64_t d, int64_t k, void* idx_o
   a.cta_b = reinterpret_cast<uint32_t*>(base + l.cta_b);
   a.fcreg = base + l.fcreg;
   a.lists = base + l.lists;
-  a.aligned = ((uintptr_t)x % 16) == 0;
+  a.aligned = ((uintptr_t)x % 32) == 0;
+  a.dbg = g_debug_stamps;
   return gp::launch_compress(dtype, a, dev, as_stream(stream));
 }
 

@@ -22,6 +22,16 @@ struct TraitsF32 {
   using Key = uint32_t;
   static constexpr int kVec = 4;        // elements per 16-byte load
   static constexpr int kKeyBits = 31;   // significant key bits (key <= 0x7F800001)
+  static constexpr int kExpBits = 8;
+  static constexpr bool kDirectT = false;  // key bits below the fine bin vary
+  static constexpr Key kInfAbs = 0x7F800000u;  // |inf| in key space; abs > kInfAbs is NaN
+  __device__ __forceinline__ static Key abs_bits(Bits b) { return b & 0x7FFFFFFFu; }
+  // key(b) >= lo_m1 + 1 (lo_m1 <= |inf| bits), as one |x| >= thr float compare; NaN -> false
+  struct Cand {
+    float thr;
+    __device__ __forceinline__ bool operator()(Bits b) const { return fabsf(__uint_as_float(b)) >= thr; }
+  };
+  __device__ __forceinline__ static Cand make_cand(Key lo_m1) { return Cand{__uint_as_float(lo_m1)}; }
   __device__ __forceinline__ static Key key(Bits b) {
     const uint32_t a = b & 0x7FFFFFFFu;
     return a > 0x7F800000u ? 0u : a + 1u;
@@ -40,6 +50,19 @@ struct TraitsBF16 {
   using Key = uint32_t;
   static constexpr int kVec = 8;
   static constexpr int kKeyBits = 31;
+  static constexpr int kExpBits = 8;
+  static constexpr bool kDirectT = true;  // 16-bit fine bin = the whole bf16 value
+  static constexpr Key kInfAbs = 0x7F800000u;
+  __device__ __forceinline__ static Key abs_bits(Bits b) { return (b & 0x7FFFu) << 16; }
+  // key >= lo_m1 + 1  <=>  ceil(lo_m1 / 2^16) <= |bits16| <= |inf|  (NaN excluded)
+  struct Cand {
+    uint32_t t16, span16;
+    __device__ __forceinline__ bool operator()(Bits b) const { return ((b & 0x7FFFu) - t16) <= span16; }
+  };
+  __device__ __forceinline__ static Cand make_cand(Key lo_m1) {
+    const uint32_t t16 = (lo_m1 + 0xFFFFu) >> 16;
+    return Cand{t16, 0x7F80u - t16};
+  }
   __device__ __forceinline__ static Key key(Bits b) {
     const uint32_t a = b & 0x7FFFu;
     return a > 0x7F80u ? 0u : (a << 16) + 1u;
@@ -57,6 +80,15 @@ struct TraitsF64 {
   using Key = uint64_t;
   static constexpr int kVec = 2;
   static constexpr int kKeyBits = 63;
+  static constexpr int kExpBits = 11;
+  static constexpr bool kDirectT = false;
+  static constexpr Key kInfAbs = 0x7FF0000000000000ull;
+  __device__ __forceinline__ static Key abs_bits(Bits b) { return b & 0x7FFFFFFFFFFFFFFFull; }
+  struct Cand {
+    double thr;
+    __device__ __forceinline__ bool operator()(Bits b) const { return fabs(__longlong_as_double((long long)b)) >= thr; }
+  };
+  __device__ __forceinline__ static Cand make_cand(Key lo_m1) { return Cand{__longlong_as_double((long long)lo_m1)}; }
   __device__ __forceinline__ static Key key(Bits b) {
     const uint64_t a = b & 0x7FFFFFFFFFFFFFFFull;
     return a > 0x7FF0000000000000ull ? 0ull : a + 1ull;
@@ -118,24 +150,29 @@ __device__ __forceinline__ uint32_t warp_incl_scan(uint32_t x) {
 
 __device__ __forceinline__ uint32_t warp_sum(uint32_t x) { return __reduce_add_sync(kFull, x); }
 
-// Grid-wide barrier for a cooperative (co-resident) launch.  Self-resetting:
-// the arrival counter returns to 0 and the generation word only increases, so
-// the workspace needs no per-call reset.  Same fence pattern as
-// cooperative_groups' grid.sync().
-__device__ __forceinline__ void grid_barrier(uint32_t* count, uint32_t* gen, uint32_t nblocks) {
+__device__ __forceinline__ uint32_t atom_add_release_gpu(uint32_t* p, uint32_t v) {
+  uint32_t old;
+  asm volatile("atom.add.release.gpu.global.u32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v) : "memory");
+  return old;
+}
+
+// Grid-wide barrier for a cooperative (co-resident) launch, one atomic per CTA.
+// CTA 0 adds 0x80000000 - (G-1), every other CTA adds 1, so the word's top bit
+// flips exactly when the last CTA arrives and the low bits return to their
+// previous value: self-resetting, nothing to clear between launches.
+// After it, data written by other CTAs before their arrival may be read with
+// plain (weak) loads: the acquire fence invalidates this SM's L1.
+__device__ __forceinline__ void fence_acq_rel_gpu() { asm volatile("fence.acq_rel.gpu;" ::: "memory"); }
+
+__device__ __forceinline__ void grid_barrier(uint32_t* word, uint32_t nblocks) {
   __syncthreads();
   if (threadIdx.x == 0) {
-    const uint32_t g = ld_acquire_gpu(gen);
-    __threadfence();
-    const uint32_t arrived = atomicAdd(count, 1u);
-    if (arrived == nblocks - 1) {
-      atomicExch(count, 0u);
-      __threadfence();
-      st_release_gpu(gen, g + 1);
-    } else {
-      while (ld_acquire_gpu(gen) == g) { __nanosleep(32); }
+    const uint32_t inc = blockIdx.x == 0 ? 0x80000000u - (nblocks - 1u) : 1u;
+    fence_acq_rel_gpu();
+    const uint32_t old = atom_add_release_gpu(word, inc);
+    while (((old ^ ld_acquire_gpu(word)) & 0x80000000u) == 0u) {
     }
-    __threadfence();
+    fence_acq_rel_gpu();
   }
   __syncthreads();
 }

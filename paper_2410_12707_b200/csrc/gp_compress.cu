@@ -10,62 +10,91 @@
 // One persistent cooperative launch, 1024 threads x one CTA per SM.  The
 // vector is split into G*32 contiguous "units", one per warp, in index order,
 // so that a warp-ordered compaction of every unit concatenated in unit order
-// is globally index ordered.
+// is globally index ordered.  A unit is read as 1 KiB rows, one 256-bit load
+// per lane per row (fully coalesced, each lane's 32 bytes contiguous).
 //
-//   stage 0  every CTA draws the same stratified 2048-element sample, builds a
-//            12-bit coarse histogram of its keys and picks a low watermark
-//            lo0 whose expected population is ~k plus a 4-sigma margin;
-//            meanwhile each warp issues a bulk L2 prefetch of its unit.
-//   stage 1  the single full read of x: every element with key >= lo0 is a
-//            candidate; candidates go into the warp's index-ordered list and a
-//            16-bit "fine" histogram (smem window, flushed to L2 by red.add).
-//            -- grid barrier B1 --
-//   stage 2  every CTA scans the global fine histogram from the top and finds
-//            the fine bin B1 holding the k-th largest key.  Keys above B1 are
-//            certainly kept ("sure"); keys inside B1 are "final candidates".
-//            Fast path (|B1| <= kFcCap): every CTA publishes its final
-//            candidates, in index order, to its own region.  -- barrier B2 --
-//   stage 3  every CTA loads the whole (small, index-ordered) final-candidate
-//            list, resolves the exact threshold key T and the tie quota by an
-//            in-smem radix select over the remaining low bits, derives its own
-//            output offset, and each warp writes its kept (index, value) pairs.
+//   stage 0  each CTA takes a low watermark lo0 from its own first two rows
+//            (4 keys per lane, no extra traffic): the key whose expected
+//            population is ~k plus a 4-sigma margin.
+//   stage 1  the single full read of x, software-pipelined (4 KiB per warp in
+//            flight): every element with |x| >= lo0 (one FSETP) is a
+//            candidate; candidates go to the warp's index-ordered list (shared
+//            memory, spilling to the workspace) and into an fb-bit "fine"
+//            histogram (smem window, flushed by red.add into one of 8 global
+//            replicas to cut same-address contention).  -- grid barrier B1 --
+//   stage 2  every CTA sums the replicas from the top and finds the fine bin
+//            B1 holding the k-th largest key.  If some CTA's watermark sat
+//            above B1, only those CTAs re-stream with a lowered watermark
+//            (one extra barrier; B1 can only move up).  Keys above B1 are kept
+//            ("sure"); keys inside B1 are final candidates (FC).
+//            Fast path (|B1| <= kFcCap): each CTA publishes its FC keys,
+//            index-ordered.  -- grid barrier B2 --
+//   stage 3  every CTA gathers the FC list, resolves the exact threshold key T
+//            and the tie quota by an in-smem radix select over the remaining
+//            low bits (bf16: nothing left, T is B1), derives its own output
+//            offset, and each warp writes its kept (index, value) pairs.
 //   slow path (|B1| > kFcCap) resolves the low bits with global per-level
 //            histograms + barriers, then one more barrier for the tie prefix.
-//   retry    if the sample overestimated lo0 (fewer than k candidates), stage 1
-//            is redone with lo0 = 0.
 //
-// All histogram state is left zeroed for the next call; the grid barrier is
-// self-resetting, so the workspace needs to be zeroed only once.
+// fb (fine-histogram bits) grows with d so |B1| stays small for large tensors.
+// All histogram state is left zeroed for the next call and the grid barrier
+// is self-resetting, so the workspace needs to be zeroed only once.
 #include <algorithm>
+#include <cmath>
+#include <type_traits>
 
 #include "gp_kernels.cuh"
 
 namespace gp {
 
+constexpr int kListBytes = 40 * 1024;  // per-CTA shared-memory candidate lists
+constexpr int kRowsPerBuf = 2;         // rows per pipeline buffer (x2 buffers in flight)
+
 // ---------------------------------------------------------------------------
 // list entries: (global index, raw bits) — 8 B for 16/32-bit, 16 B for 64-bit
 
 template <class Tr>
-__device__ __forceinline__ void store_entry(void* base, uint32_t pos, uint32_t idx, typename Tr::Bits b) {
-  if constexpr (sizeof(typename Tr::Bits) == 4) {
-    reinterpret_cast<uint2*>(base)[pos] = make_uint2(idx, (uint32_t)b);
-  } else {
-    reinterpret_cast<uint4*>(base)[pos] = make_uint4(idx, 0u, (uint32_t)b, (uint32_t)((uint64_t)b >> 32));
-  }
-}
+struct Entry {
+  static constexpr uint32_t kBytes = sizeof(typename Tr::Bits) == 4 ? 8 : 16;
+  static constexpr uint32_t kSmemCap = kListBytes / (32 * kBytes);  // entries per warp in smem
 
-template <class Tr>
-__device__ __forceinline__ void load_entry(const void* base, uint32_t pos, uint32_t& idx, typename Tr::Bits& b) {
-  if constexpr (sizeof(typename Tr::Bits) == 4) {
-    const uint2 e = __ldcg(reinterpret_cast<const uint2*>(base) + pos);
-    idx = e.x;
-    b = e.y;
-  } else {
-    const uint4 e = __ldcg(reinterpret_cast<const uint4*>(base) + pos);
-    idx = e.x;
-    b = (typename Tr::Bits)(((uint64_t)e.w << 32) | e.z);
+  __device__ __forceinline__ static void put(unsigned char* base, uint32_t pos, uint32_t idx, typename Tr::Bits b) {
+    if constexpr (kBytes == 8) {
+      reinterpret_cast<uint2*>(base)[pos] = make_uint2(idx, (uint32_t)b);
+    } else {
+      reinterpret_cast<uint4*>(base)[pos] = make_uint4(idx, 0u, (uint32_t)b, (uint32_t)((uint64_t)b >> 32));
+    }
   }
-}
+  // plain loads: global entries were written by this warp, and grid barriers
+  // (acquire fences) separate any cross-SM producer
+  __device__ __forceinline__ static void get(const unsigned char* base, uint32_t pos, uint32_t& idx,
+                                             typename Tr::Bits& b) {
+    if constexpr (kBytes == 8) {
+      const uint2 e = reinterpret_cast<const uint2*>(base)[pos];
+      idx = e.x;
+      b = e.y;
+    } else {
+      const uint4 e = reinterpret_cast<const uint4*>(base)[pos];
+      idx = e.x;
+      b = (typename Tr::Bits)(((uint64_t)e.w << 32) | e.z);
+    }
+  }
+};
+
+// A warp's candidate list: the first kSmemCap entries in shared memory, the
+// rest in the unit's workspace region (same positions).
+template <class Tr>
+struct WarpList {
+  unsigned char* smem;
+  unsigned char* glob;
+  __device__ __forceinline__ void put(uint32_t j, uint32_t idx, typename Tr::Bits b) const {
+    if (j < Entry<Tr>::kSmemCap) Entry<Tr>::put(smem, j, idx, b);
+    else Entry<Tr>::put(glob, j, idx, b);
+  }
+  __device__ __forceinline__ void get(uint32_t j, uint32_t& idx, typename Tr::Bits& b) const {
+    Entry<Tr>::get(j < Entry<Tr>::kSmemCap ? smem : glob, j, idx, b);
+  }
+};
 
 template <class Tr>
 __device__ __forceinline__ typename Tr::Bits load_bits(const void* x, uint32_t i) {
@@ -73,60 +102,94 @@ __device__ __forceinline__ typename Tr::Bits load_bits(const void* x, uint32_t i
 }
 
 // ---------------------------------------------------------------------------
-// 1024-thread block scan / crossing search
+// 32-byte lane chunks
 
-__device__ __forceinline__ uint32_t block_incl_scan(uint32_t v, uint32_t* sh32, uint32_t* total) {
+__device__ __forceinline__ void ld_chunk(const uint32_t* p, uint32_t (&v)[8]) {
+  asm volatile("ld.global.nc.L1::no_allocate.v8.u32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+               : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7])
+               : "l"(p));
+}
+
+// element e of a chunk; e may be a runtime value (select chain, no local memory)
+template <class Tr>
+__device__ __forceinline__ typename Tr::Bits chunk_elem(const uint32_t (&v)[8], uint32_t e) {
+  if constexpr (sizeof(typename Tr::Elem) == 4) {
+    uint32_t r = v[0];
+#pragma unroll
+    for (int i = 1; i < 8; ++i)
+      if (e == (uint32_t)i) r = v[i];
+    return r;
+  } else if constexpr (sizeof(typename Tr::Elem) == 2) {
+    uint32_t r = v[0];
+#pragma unroll
+    for (int i = 1; i < 8; ++i)
+      if ((e >> 1) == (uint32_t)i) r = v[i];
+    return (e & 1) ? (r >> 16) : (r & 0xFFFFu);
+  } else {
+    uint32_t lo = v[0], hi = v[1];
+#pragma unroll
+    for (int i = 1; i < 4; ++i)
+      if (e == (uint32_t)i) {
+        lo = v[2 * i];
+        hi = v[2 * i + 1];
+      }
+    return (typename Tr::Bits)(((uint64_t)hi << 32) | lo);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// scans / crossing searches
+
+// 1024-thread exclusive scan, two barriers; sh32 holds 64 words.
+__device__ __forceinline__ uint32_t block_excl_scan(uint32_t v, uint32_t* sh32, uint32_t* total) {
   const uint32_t lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const uint32_t x = warp_incl_scan(v);
   if (lane == 31) sh32[w] = x;
   __syncthreads();
-  if (w == 0) sh32[lane] = warp_incl_scan(sh32[lane]);
+  if (w == 0) sh32[32 + lane] = warp_incl_scan(sh32[lane]);
   __syncthreads();
-  const uint32_t pre = w ? sh32[w - 1] : 0u;
-  *total = sh32[31];
-  __syncthreads();
-  return x + pre;
+  *total = sh32[63];
+  return (w ? sh32[32 + w - 1] : 0u) + x - v;
 }
 
-// Thread t holds bins [4t, 4t+4) of a 4096-bin window (ascending).  Counting
-// from the top, with `base` keys already above the window, find the bin b with
-//     base + above(b) < target <= base + above(b) + h(b).
-// Returns true (in every thread) when found; outputs are block-uniform.
-__device__ __forceinline__ bool block_cross4(const uint32_t v[4], uint32_t base, uint32_t target,
-                                             uint32_t* sh32, uint32_t* sh_res, uint32_t* bin,
-                                             uint32_t* above, uint32_t* cnt, uint32_t* total) {
-  if (threadIdx.x == 0) sh_res[0] = 0u;
-  const uint32_t ts = v[0] + v[1] + v[2] + v[3];
-  uint32_t tot;
-  const uint32_t incl = block_incl_scan(ts, sh32, &tot);  // syncs order the reset above
-  uint32_t run = base + (tot - incl);
+// One warp: scanning smem bins downward from `top` to 0, 256 per step, find b
+// with above(b) < target <= above(b) + h(b).  Results are warp-uniform.
+__device__ __forceinline__ bool warp_cross_desc(const uint32_t* hist, int top, uint32_t target, uint32_t* bin,
+                                                uint32_t* above) {
+  const uint32_t lane = threadIdx.x & 31;
+  uint32_t base = 0;
+  for (int t0 = top; t0 >= 0; t0 -= 256) {
+    uint32_t v[8], s = 0;
 #pragma unroll
-  for (int b = 3; b >= 0; --b) {
-    if (run < target && run + v[b] >= target) {
-      sh_res[0] = 1u;
-      sh_res[1] = 4u * threadIdx.x + (uint32_t)b;
-      sh_res[2] = run;
-      sh_res[3] = v[b];
+    for (int i = 0; i < 8; ++i) {
+      const int b = t0 - 8 * (int)lane - i;
+      v[i] = b >= 0 ? hist[b] : 0u;
+      s += v[i];
     }
-    run += v[b];
+    const uint32_t incl = warp_incl_scan(s);
+    uint32_t run = base + incl - s;
+    const bool mine = run < target && run + s >= target;
+    const uint32_t who = __ballot_sync(kFull, mine);
+    if (who) {
+      uint32_t rb = 0, ra = 0;
+      if (mine) {
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          if (run < target && run + v[i] >= target) {
+            rb = (uint32_t)(t0 - 8 * (int)lane - i);
+            ra = run;
+          }
+          run += v[i];
+        }
+      }
+      const int src = __ffs(who) - 1;
+      *bin = __shfl_sync(kFull, rb, src);
+      *above = __shfl_sync(kFull, ra, src);
+      return true;
+    }
+    base += __shfl_sync(kFull, incl, 31);
   }
-  __syncthreads();
-  const bool found = sh_res[0] != 0u;
-  *bin = sh_res[1];
-  *above = sh_res[2];
-  *cnt = sh_res[3];
-  *total = tot;
-  __syncthreads();
-  return found;
-}
-
-__device__ __forceinline__ uint32_t hash32(uint32_t s) {
-  s ^= s >> 16;
-  s *= 0x7feb352dU;
-  s ^= s >> 15;
-  s *= 0x846ca68bU;
-  s ^= s >> 16;
-  return s;
+  return false;
 }
 
 // ---------------------------------------------------------------------------
@@ -143,6 +206,41 @@ __device__ __forceinline__ void write_out(const CompressArgs& a, uint32_t pos, u
 }
 
 // ---------------------------------------------------------------------------
+// optional stage timestamps (development aid; a.dbg is null in production)
+
+__device__ __forceinline__ unsigned long long globaltimer_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+#define STAMP(i)                                                        \
+  do {                                                                  \
+    if (a.dbg != nullptr && tid == 0) {                                 \
+      a.dbg[(size_t)c * 32 + (i)] = globaltimer_ns();                   \
+      a.dbg[(size_t)c * 32 + 16 + (i)] = (unsigned long long)clock64(); \
+    }                                                                   \
+  } while (0)
+
+// ---------------------------------------------------------------------------
+// shared-memory layout (bytes)
+
+template <class Tr>
+struct Smem {
+  static constexpr size_t coarse = 0;                                   // kCoarseBins u32
+  static constexpr size_t win = coarse + kCoarseBins * 4;               // kWinBins u32
+  static constexpr size_t low = win + kWinBins * 4;                     // kLowBins u32
+  static constexpr size_t lvl = low + kLowBins * 4;                     // 256 u32
+  static constexpr size_t s32 = lvl + 256 * 4;                          // 64 u32
+  static constexpr size_t res = s32 + 64 * 4;                           // 32 u32
+  static constexpr size_t warp = res + 32 * 4;                          // 4 x 32 u32
+  static constexpr size_t fcoff = warp + 4 * 32 * 4;                    // kMaxGrid+4 u32
+  static constexpr size_t fcpre = fcoff + (kMaxGrid + 4) * 4;           // kFcCap+4 u32
+  static constexpr size_t fckey = (fcpre + (kFcCap + 4) * 4 + 15) & ~size_t(15);  // kFcCap keys
+  static constexpr size_t list = fckey + kFcCap * sizeof(typename Tr::Key);       // kListBytes
+  static constexpr size_t total = list + kListBytes;
+};
+
+// ---------------------------------------------------------------------------
 // the kernel
 
 template <class Tr>
@@ -150,27 +248,29 @@ __global__ void __launch_bounds__(kCompressThreads, 1) compress_kernel(const Com
   using Bits = typename Tr::Bits;
   using Key = typename Tr::Key;
   using Elem = typename Tr::Elem;
-  constexpr int FS = Tr::kKeyBits - 16;  // fine bin  = key >> FS  (16 bits)
-  constexpr int CS = Tr::kKeyBits - 12;  // coarse bin = key >> CS (12 bits)
-  constexpr int VEC = Tr::kVec;
-  constexpr int U = 4;                   // 16-byte loads in flight per lane
-  constexpr size_t kEntryBytes = sizeof(Bits) == 4 ? 8 : 16;
+  using SL = Smem<Tr>;
+  constexpr int CS = Tr::kKeyBits - 12;        // coarse bin = key >> CS (12 bits)
+  constexpr int EPL = 32 / (int)sizeof(Elem);  // elements per lane chunk (8 f32, 16 bf16, 4 f64)
+  constexpr int RB = kRowsPerBuf;
+  constexpr uint32_t kEntryBytes = Entry<Tr>::kBytes;
+  const int FB = a.fb;                         // fine-histogram bits
+  const int FS = Tr::kKeyBits - FB;            // fine bin = key >> FS
+  const uint32_t nfine = 1u << FB;
 
   extern __shared__ __align__(16) unsigned char smem[];
-  uint32_t* sh_coarse = reinterpret_cast<uint32_t*>(smem);  // kCoarseBins
-  uint32_t* sh_win = sh_coarse + kCoarseBins;                // kWinBins
-  uint32_t* sh_low = sh_win + kWinBins;                      // kLowBins
-  uint32_t* sh_lvl = sh_low + kLowBins;                      // 256
-  uint32_t* sh32 = sh_lvl + 256;                             // 32
-  uint32_t* sh_res = sh32 + 32;                              // 32
-  uint32_t* w_len = sh_res + 32;                             // 32
-  uint32_t* w_a = w_len + 32;
+  uint32_t* sh_coarse = reinterpret_cast<uint32_t*>(smem + SL::coarse);
+  uint32_t* sh_win = reinterpret_cast<uint32_t*>(smem + SL::win);
+  uint32_t* sh_low = reinterpret_cast<uint32_t*>(smem + SL::low);
+  uint32_t* sh_lvl = reinterpret_cast<uint32_t*>(smem + SL::lvl);
+  uint32_t* sh32 = reinterpret_cast<uint32_t*>(smem + SL::s32);
+  uint32_t* sh_res = reinterpret_cast<uint32_t*>(smem + SL::res);
+  uint32_t* w_a = reinterpret_cast<uint32_t*>(smem + SL::warp);
   uint32_t* w_b = w_a + 32;
   uint32_t* w_aoff = w_b + 32;
   uint32_t* w_boff = w_aoff + 32;
-  uint32_t* sh_fcoff = w_boff + 32;                          // kMaxGrid + 4
-  uint32_t* sh_fcpre = sh_fcoff + kMaxGrid + 4;              // kFcCap + 4
-  Key* sh_fckey = reinterpret_cast<Key*>(sh_fcpre + kFcCap + 4);  // kFcCap
+  uint32_t* sh_fcoff = reinterpret_cast<uint32_t*>(smem + SL::fcoff);
+  uint32_t* sh_fcpre = reinterpret_cast<uint32_t*>(smem + SL::fcpre);
+  Key* sh_fckey = reinterpret_cast<Key*>(smem + SL::fckey);
 
   const uint32_t G = gridDim.x, c = blockIdx.x, tid = threadIdx.x;
   const uint32_t lane = tid & 31, w = tid >> 5;
@@ -180,183 +280,282 @@ __global__ void __launch_bounds__(kCompressThreads, 1) compress_kernel(const Com
   const uint32_t u1 = (uint32_t)min((uint64_t)u0 + a.W, (uint64_t)d);
   const uint32_t n = u1 - u0;
   const Elem* x = reinterpret_cast<const Elem*>(a.x);
-  unsigned char* my_list = reinterpret_cast<unsigned char*>(a.lists) + (size_t)unit * a.W * kEntryBytes;
+  const WarpList<Tr> list{smem + SL::list + (size_t)w * Entry<Tr>::kSmemCap * kEntryBytes,
+                          reinterpret_cast<unsigned char*>(a.lists) + (size_t)unit * a.W * kEntryBytes};
   uint32_t* ctrl = a.ctrl;
+  uint32_t* bar = &ctrl[kCtrlBar];
+  // this CTA's histogram replica (kHistCopies replicas cut same-address atomic contention)
+  uint32_t* hist = a.hist1 + (size_t)(c & (kHistCopies - 1)) * kFineBinsMax;
 
+  STAMP(0);
   if (a.header != nullptr && c == 0 && tid == 0) {
     a.header[0] = (unsigned long long)d;
     a.header[1] = (unsigned long long)k;
   }
 
-  // ---- stage 0: L2 prefetch of this warp's unit, sample-based low watermark
-  if (lane == 0 && n > 0 && a.aligned) {
-    const uint32_t bytes = (uint32_t)min((uint64_t)n * sizeof(Elem), (uint64_t)a.prefetch_bytes) & ~15u;
-    if (bytes >= 16) prefetch_l2_bulk(x + u0, bytes);
-  }
-  for (uint32_t i = tid; i < kCoarseBins; i += kCompressThreads) sh_coarse[i] = 0u;
-  if (tid == 0) sh_res[16] = 0u;
-  __syncthreads();
-  const uint32_t S = d < (uint32_t)kSamples ? d : (uint32_t)kSamples;
-  {
-    const uint32_t stride = d / S;
-    for (uint32_t s = tid; s < S; s += kCompressThreads) {
-      const uint32_t pos = (S == d) ? s : s * stride + hash32(s) % stride;
-      const Key kk = Tr::key(load_bits<Tr>(x, pos));
-      atomicAdd(&sh_coarse[(uint32_t)(kk >> CS)], 1u);
+  // ---- the unit's first two buffers (4 rows) are requested before anything else
+  const uint32_t nch = a.aligned ? n / EPL : 0u;  // full 32-byte chunks in the unit
+  const uint32_t nrow = (nch + 31) / 32;
+  const uint32_t* xw = reinterpret_cast<const uint32_t*>(x + u0);
+  uint32_t cur[RB][8], nxt[RB][8];
+  auto load_rows = [&](uint32_t(&buf)[RB][8], uint32_t r0) {
+#pragma unroll
+    for (int rr = 0; rr < RB; ++rr) {
+      const uint32_t ch = (r0 + rr) * 32u + lane;
+      if (ch < nch) {
+        ld_chunk(xw + (size_t)ch * 8, buf[rr]);
+      } else {
+#pragma unroll
+        for (int i = 0; i < 8; ++i) buf[rr][i] = 0u;
+      }
     }
+  };
+  if (nrow > 0) load_rows(cur, 0);
+  if (nrow > RB) load_rows(nxt, RB);
+
+  // ---- stage 0: low watermark from this CTA's own first rows (no extra traffic)
+  for (uint32_t i = tid; i < kCoarseBins; i += kCompressThreads) sh_coarse[i] = 0u;
+  if (tid < 32) sh_res[tid] = 0u;
+  __syncthreads();
+  {
+    uint32_t ns = 0;
+#pragma unroll
+    for (int rr = 0; rr < RB; ++rr) {
+      if ((uint32_t)rr * 32u + lane < nch) {
+        atomicAdd(&sh_coarse[(uint32_t)(Tr::key(chunk_elem<Tr>(cur[rr], 0)) >> CS)], 1u);
+        atomicAdd(&sh_coarse[(uint32_t)(Tr::key(chunk_elem<Tr>(cur[rr], EPL / 2)) >> CS)], 1u);
+        ns += 2;
+      }
+    }
+    ns = warp_sum(ns);
+    if (lane == 0 && ns) atomicAdd(&sh_res[19], ns);
   }
   __syncthreads();
   Key lo0 = 0;
   uint32_t cmax;  // highest non-empty coarse bin of the sample
   {
-    uint32_t v[4], m = 0;
+    const uint32_t S = sh_res[19];
+    uint32_t v[4], m = 0, ts = 0;
 #pragma unroll
     for (int b = 0; b < 4; ++b) {
       v[b] = sh_coarse[4 * tid + b];
       if (v[b]) m = 4 * tid + b + 1;
+      ts += v[b];
     }
     m = __reduce_max_sync(kFull, m);
     if (lane == 0 && m) atomicMax(&sh_res[16], m);
     const double mu = (double)S * (double)k / (double)d;
-    const double rs = ceil(mu + 4.0 * sqrt(mu) + 4.0);
-    const bool want = rs < (double)S;
-    uint32_t bin, above, cnt, tot;
-    const bool found = block_cross4(v, 0u, want ? (uint32_t)rs : 0xFFFFFFFFu, sh32, sh_res, &bin, &above, &cnt, &tot);
-    if (want && found) lo0 = (Key)bin << CS;
-    cmax = sh_res[16] ? sh_res[16] - 1 : 0u;
-  }
-  const uint32_t top = min((uint32_t)kFineBins, ((cmax + 1u) << 4) + 512u);
-
-  uint32_t L = 0;              // this warp's candidate count
-  uint32_t B1 = 0, G1 = 0, M = 0, lobin = 0, maxb = 0;
-  for (int attempt = 0;; ++attempt) {
-    if (attempt == 1) lo0 = 0;
-    lobin = (uint32_t)(lo0 >> FS);
-    uint32_t wb = top > (uint32_t)kWinBins ? top - kWinBins : 0u;
-    wb = max(wb, lobin);
-    wb = min(wb, (uint32_t)(kFineBins - kWinBins));
-    const uint32_t lowlim = min((uint32_t)kLowBins, wb);
-
-    for (uint32_t i = tid; i < kWinBins; i += kCompressThreads) sh_win[i] = 0u;
-    if (tid < kLowBins) sh_low[tid] = 0u;
-    if (tid == 0) sh_res[17] = 0u;
-    __syncthreads();
-
-    // ---- stage 1: the one full pass over x
-    L = 0;
-    uint32_t mymax = 0;  // 1 + highest fine bin among my candidates
-    auto hist_add = [&](uint32_t fb) {
-      const uint32_t off = fb - wb;
-      if (off < (uint32_t)kWinBins) atomicAdd(&sh_win[off], 1u);
-      else if (fb < lowlim) atomicAdd(&sh_low[fb], 1u);
-      else atomicAdd(&a.hist1[fb], 1u);
-      mymax = max(mymax, fb + 1u);
-    };
-    const uint32_t nv = a.aligned ? n / VEC : 0u;
-    const uint4* xv = reinterpret_cast<const uint4*>(x + u0);
-    for (uint32_t v0 = 0; v0 < nv; v0 += 32u * U) {
-      uint4 r[U];
+    const double rs = ceil(mu + 4.0 * sqrt(mu) + 8.0);
+    uint32_t tot;
+    const uint32_t excl = block_excl_scan(ts, sh32, &tot);
+    if (rs < (double)S) {
+      const uint32_t target = (uint32_t)rs;
+      uint32_t run = tot - excl - ts;  // sample count in bins above this thread's
 #pragma unroll
-      for (int q = 0; q < U; ++q) {
-        const uint32_t vi = v0 + q * 32u + lane;
-        r[q] = vi < nv ? ld_stream_v4(xv + vi) : make_uint4(0u, 0u, 0u, 0u);
-      }
-#pragma unroll
-      for (int q = 0; q < U; ++q) {
-        const uint32_t vi = v0 + q * 32u + lane;
-        uint32_t flags = 0;
-        if (vi < nv) {
-#pragma unroll
-          for (int e = 0; e < VEC; ++e)
-            if (Tr::key(Tr::lane(r[q], e)) >= lo0) flags |= 1u << e;
-        }
-        if (__any_sync(kFull, flags)) {
-          const uint32_t cnt = __popc(flags);
-          const uint32_t incl = warp_incl_scan(cnt);
-          uint32_t pos = L + incl - cnt;
-#pragma unroll
-          for (int e = 0; e < VEC; ++e) {
-            if ((flags >> e) & 1u) {
-              const Bits b = Tr::lane(r[q], e);
-              hist_add((uint32_t)(Tr::key(b) >> FS));
-              store_entry<Tr>(my_list, pos++, u0 + vi * VEC + e, b);
-            }
-          }
-          L += __shfl_sync(kFull, incl, 31);
-        }
+      for (int b = 3; b >= 0; --b) {
+        if (run < target && run + v[b] >= target) sh_res[17] = 4 * tid + b + 1;
+        run += v[b];
       }
     }
-    for (uint32_t i0 = nv * VEC; i0 < n; i0 += 32u) {  // scalar tail / unaligned input
+    __syncthreads();
+    if (sh_res[17]) lo0 = (Key)(sh_res[17] - 1) << CS;
+    cmax = sh_res[16] ? sh_res[16] - 1 : (uint32_t)(kCoarseBins - 1);
+  }
+  // top of the smem histogram window: two exponents above the sample maximum
+  const uint32_t top = min(nfine, ((cmax + 1u) << (FB - 12)) + (2u << (FB - Tr::kExpBits)));
+
+  STAMP(1);
+  uint32_t L = 0;                              // this warp's candidate count
+  uint32_t my_lobin = (uint32_t)(lo0 >> FS);   // lowest fine bin this CTA histograms
+  uint32_t my_maxb = 0;                        // 1 + highest fine bin this CTA histogrammed
+
+  // ---- stage 1 (and the rare rescan): stream the unit, keep keys >= lo and
+  // histogram those whose fine bin is below add_below
+  auto stream_unit = [&](Key lo, uint32_t add_below, bool preloaded) {
+    const uint32_t lob = (uint32_t)(lo >> FS);
+    uint32_t wb = top > (uint32_t)kWinBins ? top - kWinBins : 0u;
+    wb = max(wb, lob);
+    wb = min(wb, nfine - kWinBins);
+    const uint32_t lowlim = min((uint32_t)kLowBins, wb);
+    for (uint32_t i = tid; i < kWinBins; i += kCompressThreads) sh_win[i] = 0u;
+    if (tid < kLowBins) sh_low[tid] = 0u;
+    if (tid == 0) {
+      sh_res[18] = 0u;
+      sh_res[20] = 0u;
+    }
+    __syncthreads();
+    L = 0;
+    uint32_t mymax = 0;
+    const Key lo_m1 = lo ? lo - 1 : (Key)0;
+    auto take = [&](uint32_t pos, uint32_t idx, Bits b) {
+      const uint32_t fb = (uint32_t)(Tr::key(b) >> FS);
+      if (fb < add_below) {
+        const uint32_t off = fb - wb;
+        if (off < (uint32_t)kWinBins) atomicAdd(&sh_win[off], 1u);
+        else if (fb < lowlim) atomicAdd(&sh_low[fb], 1u);
+        else atomicAdd(&hist[fb], 1u);
+        mymax = max(mymax, fb + 1u);
+      }
+      list.put(pos, idx, b);
+    };
+    // Candidate test in the value domain: one |x| >= thr compare per element
+    // (FSETP/DSETP with the abs modifier; NaN compares false, its key is 0).
+    const typename Tr::Cand test = Tr::make_cand(lo_m1);
+    auto process = [&](const uint32_t(&buf)[RB][8], uint32_t r0, auto all_tag) {
+      constexpr bool kAll = decltype(all_tag)::value;  // lo == 0: every element, NaN included
+      uint32_t m[RB];
+#pragma unroll
+      for (int rr = 0; rr < RB; ++rr) {
+        uint32_t mm = 0;
+#pragma unroll
+        for (int e = 0; e < EPL; ++e)
+          if (kAll || test(chunk_elem<Tr>(buf[rr], e))) mm |= 1u << e;
+        m[rr] = ((r0 + rr) * 32u + lane < nch) ? mm : 0u;
+      }
+      static_assert(RB == 2, "packed two-row scan");
+      const uint32_t packed = __popc(m[0]) | (__popc(m[1]) << 16);
+      if (__any_sync(kFull, packed)) {
+        const uint32_t incl = warp_incl_scan(packed);
+        const uint32_t excl = incl - packed, tot = __shfl_sync(kFull, incl, 31);
+        uint32_t pos[RB] = {L + (excl & 0xFFFFu), L + (tot & 0xFFFFu) + (excl >> 16)};
+        L += (tot & 0xFFFFu) + (tot >> 16);
+#pragma unroll
+        for (int rr = 0; rr < RB; ++rr) {
+          uint32_t mm = m[rr];
+          const uint32_t base = u0 + ((r0 + rr) * 32u + lane) * EPL;
+          while (mm) {
+            const uint32_t e = __ffs(mm) - 1;
+            mm &= mm - 1;
+            take(pos[rr]++, base + e, chunk_elem<Tr>(buf[rr], e));
+          }
+        }
+      }
+    };
+    if (!preloaded) {
+      if (nrow > 0) load_rows(cur, 0);
+      if (nrow > RB) load_rows(nxt, RB);
+    }
+    // two buffers in flight: while one is being filtered the other is loading
+    auto stream_rows = [&](auto all_tag) {
+      for (uint32_t r0 = 0; r0 < nrow; r0 += 2 * RB) {
+        process(cur, r0, all_tag);
+        if (r0 + 2 * RB < nrow) load_rows(cur, r0 + 2 * RB);
+        if (r0 + RB < nrow) {
+          process(nxt, r0 + RB, all_tag);
+          if (r0 + 3 * RB < nrow) load_rows(nxt, r0 + 3 * RB);
+        }
+      }
+    };
+    if (lo == 0) stream_rows(std::true_type{});
+    else stream_rows(std::false_type{});
+    const Key span = lo ? Tr::kInfAbs - lo_m1 : ~(Key)0;
+    for (uint32_t i0 = nch * EPL; i0 < n; i0 += 32u) {  // scalar tail / unaligned input
       const uint32_t i = i0 + lane;
       Bits b = 0;
       bool f = false;
       if (i < n) {
         b = load_bits<Tr>(x, u0 + i);
-        f = Tr::key(b) >= lo0;
+        f = (Key)(Tr::abs_bits(b) - lo_m1) <= span;
       }
-      const uint32_t m = __ballot_sync(kFull, f);
-      if (f) {
-        hist_add((uint32_t)(Tr::key(b) >> FS));
-        store_entry<Tr>(my_list, L + __popc(m & lanemask_lt()), u0 + i, b);
-      }
-      L += __popc(m);
+      const uint32_t mk = __ballot_sync(kFull, f);
+      if (f) take(L + __popc(mk & lanemask_lt()), u0 + i, b);
+      L += __popc(mk);
     }
     mymax = __reduce_max_sync(kFull, mymax);
-    if (lane == 0 && mymax) atomicMax(&sh_res[17], mymax);
+    if (lane == 0) {
+      if (mymax) atomicMax(&sh_res[18], mymax);
+      if (L) atomicAdd(&sh_res[20], L);
+    }
     __syncthreads();
+    my_maxb = max(my_maxb, sh_res[18]);
     for (uint32_t i = tid; i < kWinBins; i += kCompressThreads) {
       const uint32_t v = sh_win[i];
-      if (v) red_add_gpu(&a.hist1[wb + i], v);
+      if (v) red_add_gpu(&hist[wb + i], v);
     }
-    if (tid < lowlim && sh_low[tid]) red_add_gpu(&a.hist1[tid], sh_low[tid]);
-    if (tid == 0 && sh_res[17]) atomicMax(&ctrl[kCtrlMaxBin], sh_res[17]);
-    grid_barrier(&ctrl[kCtrlBarCount], &ctrl[kCtrlBarGen], G);  // ---- B1
+    if (tid < lowlim && sh_low[tid]) red_add_gpu(&hist[tid], sh_low[tid]);
+    if (tid == 0) {
+      if (sh_res[18]) atomicMax(&ctrl[kCtrlMaxBin], sh_res[18]);
+      if (sh_res[20]) red_add_gpu(&ctrl[kCtrlCands], sh_res[20]);
+    }
+  };
 
-    // ---- stage 2: locate the fine bin B1 that holds the k-th largest key
-    maxb = __ldcg(&ctrl[kCtrlMaxBin]);
-    bool found = false;
-    {
-      uint32_t base = 0;
-      int hi = (int)maxb - 1;
-      while (!found && hi >= (int)lobin) {
-        const int cb = hi - 4095;
-        uint32_t v[4];
+  // ---- stage 2 helper: sum the replicas from the top, 4096 bins per step,
+  // and find the fine bin holding the k-th largest key
+  uint32_t B1 = 0, G1 = 0, M = 0;
+  auto find_b1 = [&]() -> bool {
+    const uint32_t mb = ctrl[kCtrlMaxBin];
+    const int lowest = (int)(0xFFFFFFFFu - ctrl[kCtrlMinLoBin]);  // no bin below any watermark is populated
+    if (tid == 0) sh_res[0] = 0u;
+    uint32_t base = 0;
+    for (int t0 = (int)mb - 1; t0 >= lowest; t0 -= 4 * kCompressThreads) {
+      uint32_t v[4], s = 0;
 #pragma unroll
-        for (int b = 0; b < 4; ++b) {
-          const int bin = cb + 4 * (int)tid + b;
-          v[b] = (bin >= (int)lobin && bin <= hi) ? __ldcg(&a.hist1[bin]) : 0u;
+      for (int b = 0; b < 4; ++b) {  // thread order = descending bins
+        const int bin = t0 - 4 * (int)tid - b;
+        v[b] = 0;
+        if (bin >= lowest) {
+#pragma unroll
+          for (int r = 0; r < kHistCopies; ++r) v[b] += a.hist1[(size_t)r * kFineBinsMax + bin];
         }
-        uint32_t bin, above, cnt, tot;
-        found = block_cross4(v, base, k, sh32, sh_res, &bin, &above, &cnt, &tot);
-        if (found) {
-          B1 = (uint32_t)(cb + (int)bin);
-          G1 = above;
-          M = cnt;
-        }
-        base += tot;
-        hi = cb - 1;
+        s += v[b];
       }
+      uint32_t tot;
+      uint32_t run = base + block_excl_scan(s, sh32, &tot);  // keys in higher bins
+#pragma unroll
+      for (int b = 0; b < 4; ++b) {
+        if (run < k && run + v[b] >= k) {
+          sh_res[0] = 1u;
+          sh_res[1] = (uint32_t)(t0 - 4 * (int)tid - b);
+          sh_res[2] = run;
+          sh_res[3] = v[b];
+        }
+        run += v[b];
+      }
+      __syncthreads();
+      if (sh_res[0]) break;
+      base += tot;
     }
-    if (found) break;
-    // lo0 overestimated: clear and redo stage 1 with every element a candidate
-    grid_barrier(&ctrl[kCtrlBarCount], &ctrl[kCtrlBarGen], G);
-    {
-      const uint32_t span = maxb > lobin ? maxb - lobin : 0u;
-      const uint32_t z0 = lobin + (uint32_t)(((uint64_t)span * c) / G);
-      const uint32_t z1 = lobin + (uint32_t)(((uint64_t)span * (c + 1)) / G);
-      for (uint32_t i = z0 + tid; i < z1; i += kCompressThreads) a.hist1[i] = 0u;
-      if (c == 0 && tid == 0) ctrl[kCtrlMaxBin] = 0u;
-    }
-    grid_barrier(&ctrl[kCtrlBarCount], &ctrl[kCtrlBarGen], G);
-  }
+    B1 = sh_res[1];
+    G1 = sh_res[2];
+    M = sh_res[3];
+    return sh_res[0] != 0u;
+  };
 
-  // per-warp split of my candidates: sure (fine bin > B1) / final (== B1)
+  stream_unit(lo0, 0xFFFFFFFFu, true);
+  if (tid == 0) {
+    atomicMax(&ctrl[kCtrlMaxLoBin], my_lobin + 1u);
+    atomicMax(&ctrl[kCtrlMinLoBin], 0xFFFFFFFFu - my_lobin);  // min, stored complemented
+  }
+  STAMP(2);
+  grid_barrier(bar, G);  // ---- B1
+  STAMP(3);
+  {
+    const bool enough = ctrl[kCtrlCands] >= k;
+    const bool found = enough && find_b1();
+    const uint32_t maxlob = ctrl[kCtrlMaxLoBin] - 1u;
+    if (!found || maxlob > B1) {
+      // Some CTA's watermark sat above B1 (or too few candidates overall):
+      // only those CTAs re-stream their chunk with the watermark lowered to
+      // B1's edge, adding just the newly covered bins; B1 can only move up.
+      const uint32_t b1e = found ? B1 : 0u;
+      if (my_lobin > b1e) {
+        stream_unit((Key)b1e << FS, my_lobin, false);
+        my_lobin = b1e;
+        if (tid == 0) atomicMax(&ctrl[kCtrlMinLoBin], 0xFFFFFFFFu - b1e);
+      }
+      grid_barrier(bar, G);
+      find_b1();
+    }
+  }
+  STAMP(4);
+
+  // per-warp split of my candidates: sure (fine bin > B1) / final candidates (== B1)
   {
     uint32_t ca = 0, cb = 0;
     for (uint32_t j = lane; j < L; j += 32u) {
       uint32_t idx;
       Bits b;
-      load_entry<Tr>(my_list, j, idx, b);
+      list.get(j, idx, b);
       const uint32_t fb = (uint32_t)(Tr::key(b) >> FS);
       ca += fb > B1;
       cb += fb == B1;
@@ -380,11 +579,14 @@ __global__ void __launch_bounds__(kCompressThreads, 1) compress_kernel(const Com
     }
   }
   __syncthreads();
+  // bf16: the bits below the fine bin are constant, so B1 already is the key
+  // (except bin 0, which holds both NaN, key 0, and +-0, key 1)
+  const bool kDirectT = Tr::kDirectT && B1 != 0;
 
   if (M <= (uint32_t)kFcCap) {
     // ================= fast path =================
-    Key* fcreg = reinterpret_cast<Key*>(a.fcreg) + (size_t)c * kFcCap;
-    {
+    if (!kDirectT) {
+      Key* fcreg = reinterpret_cast<Key*>(a.fcreg) + (size_t)c * kFcCap;
       uint32_t j0 = w_boff[w];
       for (uint32_t base = 0; base < L; base += 32u) {
         const uint32_t j = base + lane;
@@ -393,73 +595,120 @@ __global__ void __launch_bounds__(kCompressThreads, 1) compress_kernel(const Com
         if (j < L) {
           uint32_t idx;
           Bits b;
-          load_entry<Tr>(my_list, j, idx, b);
+          list.get(j, idx, b);
           kk = Tr::key(b);
           isfc = (uint32_t)(kk >> FS) == B1;
         }
-        const uint32_t m = __ballot_sync(kFull, isfc);
-        if (isfc) fcreg[j0 + __popc(m & lanemask_lt())] = kk;
-        j0 += __popc(m);
+        const uint32_t mk = __ballot_sync(kFull, isfc);
+        if (isfc) fcreg[j0 + __popc(mk & lanemask_lt())] = kk;
+        j0 += __popc(mk);
       }
     }
     if (tid == 0) {
       a.cta_a[c] = sh_res[8];
       a.cta_b[c] = sh_res[9];
     }
-    grid_barrier(&ctrl[kCtrlBarCount], &ctrl[kCtrlBarGen], G);  // ---- B2
+    STAMP(5);
+    grid_barrier(bar, G);  // ---- B2
+    STAMP(6);
 
-    // ---- stage 3: exact threshold inside B1, offsets, output
-    {
-      const uint32_t va = tid < G ? __ldcg(&a.cta_a[tid]) : 0u;
-      const uint32_t vb = tid < G ? __ldcg(&a.cta_b[tid]) : 0u;
-      uint32_t ta, tb;
-      const uint32_t ia = block_incl_scan(va, sh32, &ta);
-      const uint32_t ib = block_incl_scan(vb, sh32, &tb);
-      if (tid < G) sh_fcoff[tid] = ib - vb;
-      if (tid == 0) sh_fcoff[G] = tb;
-      if (tid == c) sh_res[10] = ia - va;
+    // ---- stage 3: per-CTA prefixes (warp 0), FC list into smem (all warps)
+    uint32_t* tmp_a = sh_fcpre;  // scratch until the FC prefix is built
+    if (tid < G) {               // one global round trip for all per-CTA counts
+      tmp_a[tid] = a.cta_a[tid];
+      sh_fcoff[tid] = a.cta_b[tid];
+    }
+    __syncthreads();
+    if (w == 0) {
+      const uint32_t per = (G + 31) / 32;
+      uint32_t sa = 0, sb = 0;
+      for (uint32_t i = 0; i < per; ++i) {
+        const uint32_t c2 = lane * per + i;
+        if (c2 < G) {
+          sa += tmp_a[c2];
+          sb += sh_fcoff[c2];
+        }
+      }
+      const uint32_t ia = warp_incl_scan(sa), ib = warp_incl_scan(sb);
+      uint32_t ra = ia - sa, rb = ib - sb;
+      for (uint32_t i = 0; i < per; ++i) {
+        const uint32_t c2 = lane * per + i;
+        if (c2 < G) {
+          const uint32_t va = tmp_a[c2], vb = sh_fcoff[c2];
+          if (c2 == c) sh_res[10] = ra;
+          sh_fcoff[c2] = rb;
+          ra += va;
+          rb += vb;
+        }
+      }
+      if (lane == 31) sh_fcoff[G] = ib;
     }
     __syncthreads();
     const uint32_t Mt = sh_fcoff[G];
     const uint32_t sure_off = sh_res[10];
-    for (uint32_t p = tid; p < Mt; p += kCompressThreads) {
-      uint32_t lo = 0, hi = G - 1;
-      while (lo < hi) {
-        const uint32_t mid = (lo + hi + 1) >> 1;
-        if (sh_fcoff[mid] <= p) lo = mid;
-        else hi = mid - 1;
-      }
-      sh_fckey[p] = __ldcg(reinterpret_cast<const Key*>(a.fcreg) + (size_t)lo * kFcCap + (p - sh_fcoff[lo]));
-    }
-    __syncthreads();
-    // in-smem radix select over the low FS bits of the final candidates
     uint32_t need = k - G1;
     Key T = (Key)B1 << FS;
-    for (int hib = FS; hib > 0;) {
-      const int nb = hib < 8 ? hib : 8;
-      const int lob = hib - nb;
-      if (tid < 256) sh_lvl[tid] = 0u;
-      __syncthreads();
-      for (uint32_t p = tid; p < Mt; p += kCompressThreads) {
-        const Key kk = sh_fckey[p];
-        if ((kk >> hib) == (T >> hib)) atomicAdd(&sh_lvl[(uint32_t)(kk >> lob) & ((1u << nb) - 1u)], 1u);
+    if (kDirectT) {
+      T |= 1;  // every FC key equals T; the tie quota is the whole need
+    } else {
+      {
+        // gather the index-ordered FC list: position p belongs to the last CTA
+        // whose FC offset is <= p; all loads are issued before any store
+        constexpr int R = kFcCap / kCompressThreads;
+        Key kv[R];
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+          const uint32_t p = tid + r * kCompressThreads;
+          if (p < Mt) {
+            uint32_t lo = 0, hi = G - 1;
+            while (lo < hi) {
+              const uint32_t mid = (lo + hi + 1) >> 1;
+              if (sh_fcoff[mid] <= p) lo = mid;
+              else hi = mid - 1;
+            }
+            kv[r] = reinterpret_cast<const Key*>(a.fcreg)[(size_t)lo * kFcCap + (p - sh_fcoff[lo])];
+          }
+        }
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+          const uint32_t p = tid + r * kCompressThreads;
+          if (p < Mt) sh_fckey[p] = kv[r];
+        }
       }
       __syncthreads();
-      uint32_t v[4];
-#pragma unroll
-      for (int b = 0; b < 4; ++b) v[b] = (4 * tid + b < 256u) ? sh_lvl[4 * tid + b] : 0u;
-      uint32_t dig, above, cnt, tot;
-      block_cross4(v, 0u, need, sh32, sh_res, &dig, &above, &cnt, &tot);
-      T |= (Key)dig << lob;
-      need -= above;
-      hib = lob;
+      // in-smem radix select over the low FS bits of the final candidates
+      for (int hib = FS; hib > 0;) {
+        const int nb = hib < 8 ? hib : 8;
+        const int lob = hib - nb;
+        if (tid < 256) sh_lvl[tid] = 0u;
+        __syncthreads();
+        for (uint32_t p = tid; p < Mt; p += kCompressThreads) {
+          const Key kk = sh_fckey[p];
+          if ((kk >> hib) == (T >> hib)) atomicAdd(&sh_lvl[(uint32_t)(kk >> lob) & ((1u << nb) - 1u)], 1u);
+        }
+        __syncthreads();
+        if (w == 0) {
+          uint32_t dig = 0, above = 0;
+          warp_cross_desc(sh_lvl, (1 << nb) - 1, need, &dig, &above);
+          if (lane == 0) {
+            sh_res[12] = dig;
+            sh_res[13] = above;
+          }
+        }
+        __syncthreads();
+        T |= (Key)sh_res[12] << lob;
+        need -= sh_res[13];
+        hib = lob;
+      }
     }
     const uint32_t need_eq = need;  // number of key == T final candidates kept
-    {
-      uint32_t pk[4], s = 0;
+    STAMP(7);
+    if (!kDirectT) {
+      constexpr int PER = kFcCap / kCompressThreads;
+      uint32_t pk[PER], s = 0;
 #pragma unroll
-      for (int b = 0; b < 4; ++b) {
-        const uint32_t p = 4 * tid + b;
+      for (int b = 0; b < PER; ++b) {
+        const uint32_t p = PER * tid + b;
         uint32_t v = 0;
         if (p < Mt) {
           const Key kk = sh_fckey[p];
@@ -469,16 +718,18 @@ __global__ void __launch_bounds__(kCompressThreads, 1) compress_kernel(const Com
         s += v;
       }
       uint32_t tot;
-      uint32_t run = block_incl_scan(s, sh32, &tot) - s;
+      uint32_t run = block_excl_scan(s, sh32, &tot);
 #pragma unroll
-      for (int b = 0; b < 4; ++b) {
-        sh_fcpre[4 * tid + b] = run;
+      for (int b = 0; b < PER; ++b) {
+        sh_fcpre[PER * tid + b] = run;
         run += pk[b];
       }
       if (tid == 0) sh_fcpre[kFcCap] = tot;
+      __syncthreads();
     }
-    __syncthreads();
+    // kept final candidates before FC position p
     auto fcsel = [&](uint32_t p) {
+      if (kDirectT) return min(p, need_eq);
       const uint32_t v = sh_fcpre[p];
       return (v >> 16) + min(v & 0xFFFFu, need_eq);
     };
@@ -494,14 +745,17 @@ __global__ void __launch_bounds__(kCompressThreads, 1) compress_kernel(const Com
       uint32_t fb = 0;
       const bool valid = j < L;
       if (valid) {
-        load_entry<Tr>(my_list, j, idx, b);
+        list.get(j, idx, b);
         kk = Tr::key(b);
         fb = (uint32_t)(kk >> FS);
       }
       const bool isfc = valid && fb == B1;
       const uint32_t fm = __ballot_sync(kFull, isfc);
       const uint32_t p = jfc + __popc(fm & lanemask_lt());
-      const bool sel = valid && (fb > B1 || (isfc && (kk > T || (kk == T && (sh_fcpre[p] & 0xFFFFu) < need_eq))));
+      bool keep_fc;
+      if (kDirectT) keep_fc = p < need_eq;
+      else keep_fc = kk > T || (kk == T && (sh_fcpre[p] & 0xFFFFu) < need_eq);
+      const bool sel = valid && (fb > B1 || (isfc && keep_fc));
       const uint32_t sm = __ballot_sync(kFull, sel);
       if (sel) write_out<Tr>(a, o + __popc(sm & lanemask_lt()), idx, b);
       o += __popc(sm);
@@ -512,29 +766,39 @@ __global__ void __launch_bounds__(kCompressThreads, 1) compress_kernel(const Com
     uint32_t need = k - G1;
     Key T = (Key)B1 << FS;
     int lvl = 0;
-    for (int hib = FS; hib > 0; ++lvl) {
-      const int nb = hib < 8 ? hib : 8;
-      const int lob = hib - nb;
-      if (tid < 256) sh_lvl[tid] = 0u;
-      __syncthreads();
-      for (uint32_t j = lane; j < L; j += 32u) {
-        uint32_t idx;
-        Bits b;
-        load_entry<Tr>(my_list, j, idx, b);
-        const Key kk = Tr::key(b);
-        if ((kk >> hib) == (T >> hib)) atomicAdd(&sh_lvl[(uint32_t)(kk >> lob) & ((1u << nb) - 1u)], 1u);
+    if (kDirectT) {
+      T |= 1;
+    } else {
+      for (int hib = FS; hib > 0; ++lvl) {
+        const int nb = hib < 8 ? hib : 8;
+        const int lob = hib - nb;
+        if (tid < 256) sh_lvl[tid] = 0u;
+        __syncthreads();
+        for (uint32_t j = lane; j < L; j += 32u) {
+          uint32_t idx;
+          Bits b;
+          list.get(j, idx, b);
+          const Key kk = Tr::key(b);
+          if ((kk >> hib) == (T >> hib)) atomicAdd(&sh_lvl[(uint32_t)(kk >> lob) & ((1u << nb) - 1u)], 1u);
+        }
+        __syncthreads();
+        if (tid < 256 && sh_lvl[tid]) red_add_gpu(&a.hist_lvl[lvl * 256 + tid], sh_lvl[tid]);
+        grid_barrier(bar, G);
+        if (tid < 256) sh_lvl[tid] = a.hist_lvl[lvl * 256 + tid];
+        __syncthreads();
+        if (w == 0) {
+          uint32_t dig = 0, above = 0;
+          warp_cross_desc(sh_lvl, (1 << nb) - 1, need, &dig, &above);
+          if (lane == 0) {
+            sh_res[12] = dig;
+            sh_res[13] = above;
+          }
+        }
+        __syncthreads();
+        T |= (Key)sh_res[12] << lob;
+        need -= sh_res[13];
+        hib = lob;
       }
-      __syncthreads();
-      if (tid < 256 && sh_lvl[tid]) red_add_gpu(&a.hist_lvl[lvl * 256 + tid], sh_lvl[tid]);
-      grid_barrier(&ctrl[kCtrlBarCount], &ctrl[kCtrlBarGen], G);
-      uint32_t v[4];
-#pragma unroll
-      for (int b = 0; b < 4; ++b) v[b] = (4 * tid + b < 256u) ? __ldcg(&a.hist_lvl[lvl * 256 + 4 * tid + b]) : 0u;
-      uint32_t dig, above, cnt, tot;
-      block_cross4(v, 0u, need, sh32, sh_res, &dig, &above, &cnt, &tot);
-      T |= (Key)dig << lob;
-      need -= above;
-      hib = lob;
     }
     const uint32_t need_eq = need;
     {
@@ -542,7 +806,7 @@ __global__ void __launch_bounds__(kCompressThreads, 1) compress_kernel(const Com
       for (uint32_t j = lane; j < L; j += 32u) {
         uint32_t idx;
         Bits b;
-        load_entry<Tr>(my_list, j, idx, b);
+        list.get(j, idx, b);
         const Key kk = Tr::key(b);
         gt += kk > T;
         eq += kk == T;
@@ -565,16 +829,16 @@ __global__ void __launch_bounds__(kCompressThreads, 1) compress_kernel(const Com
         a.cta_b[c] = ib;
       }
     }
-    grid_barrier(&ctrl[kCtrlBarCount], &ctrl[kCtrlBarGen], G);
+    grid_barrier(bar, G);
     {
-      const uint32_t va = tid < G ? __ldcg(&a.cta_a[tid]) : 0u;
-      const uint32_t vb = tid < G ? __ldcg(&a.cta_b[tid]) : 0u;
+      const uint32_t va = tid < G ? a.cta_a[tid] : 0u;
+      const uint32_t vb = tid < G ? a.cta_b[tid] : 0u;
       uint32_t ta, tb;
-      const uint32_t ia = block_incl_scan(va, sh32, &ta);
-      const uint32_t ib = block_incl_scan(vb, sh32, &tb);
+      const uint32_t ea = block_excl_scan(va, sh32, &ta);
+      const uint32_t eb = block_excl_scan(vb, sh32, &tb);
       if (tid == c) {
-        sh_res[10] = ia - va;
-        sh_res[11] = ib - vb;
+        sh_res[10] = ea;
+        sh_res[11] = eb;
       }
     }
     __syncthreads();
@@ -589,7 +853,7 @@ __global__ void __launch_bounds__(kCompressThreads, 1) compress_kernel(const Com
       Key kk = 0;
       const bool valid = j < L;
       if (valid) {
-        load_entry<Tr>(my_list, j, idx, b);
+        list.get(j, idx, b);
         kk = Tr::key(b);
       }
       const bool iseq = valid && kk == T;
@@ -604,16 +868,17 @@ __global__ void __launch_bounds__(kCompressThreads, 1) compress_kernel(const Com
       for (uint32_t i = tid; i < (uint32_t)(lvl * 256); i += kCompressThreads) a.hist_lvl[i] = 0u;
     }
   }
+  STAMP(8);
 
-  // ---- leave the workspace clean: every histogram bin that can be non-zero
-  // lies in [lobin, maxb); all reads of hist1 / maxbin happened before the
-  // last barrier.
-  {
-    const uint32_t span = maxb > lobin ? maxb - lobin : 0u;
-    const uint32_t z0 = lobin + (uint32_t)(((uint64_t)span * c) / G);
-    const uint32_t z1 = lobin + (uint32_t)(((uint64_t)span * (c + 1)) / G);
-    for (uint32_t i = z0 + tid; i < z1; i += kCompressThreads) a.hist1[i] = 0u;
-    if (c == 0 && tid == 0) ctrl[kCtrlMaxBin] = 0u;
+  // ---- leave the workspace clean: every bin this CTA added to its histogram
+  // replica lies in [my_lobin, my_maxb); all histogram / control reads
+  // happened before the last grid barrier.
+  for (uint32_t i = my_lobin + tid; i < my_maxb; i += kCompressThreads) hist[i] = 0u;
+  if (c == 0 && tid == 0) {
+    ctrl[kCtrlMaxBin] = 0u;
+    ctrl[kCtrlMaxLoBin] = 0u;
+    ctrl[kCtrlMinLoBin] = 0u;
+    ctrl[kCtrlCands] = 0u;
   }
 }
 
@@ -631,10 +896,14 @@ __global__ void __launch_bounds__(256) keep_all_kernel(const CompressArgs a) {
 // ---------------------------------------------------------------------------
 // host side
 
+// Fine-histogram resolution: 16 bits up to 2^23 elements, +1 bit per doubling
+// (max 20), so the population of the threshold bin stays roughly constant.
 template <class Tr>
-static size_t compress_smem_bytes() {
-  return (size_t)(kCoarseBins + kWinBins + kLowBins + 256 + 32 * 8 + kMaxGrid + 4 + kFcCap + 4) * 4 +
-         (size_t)kFcCap * sizeof(typename Tr::Key);
+static int fine_bits(uint64_t d) {
+  if (Tr::kDirectT) return 16;
+  int fb = 16;
+  while (fb < kFineBitsMax && (d >> (fb + 7)) != 0) ++fb;
+  return fb;
 }
 
 template <class Tr>
@@ -646,7 +915,7 @@ static int launch_compress_t(CompressArgs a, const DeviceInfo& dev, cudaStream_t
   }
   static int configured[64] = {0};
   static int max_blocks_per_sm[64] = {0};
-  const size_t smem = compress_smem_bytes<Tr>();
+  const size_t smem = Smem<Tr>::total;
   if (!configured[dev.ordinal]) {
     if (cudaFuncSetAttribute(compress_kernel<Tr>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
       return 5;
@@ -658,13 +927,11 @@ static int launch_compress_t(CompressArgs a, const DeviceInfo& dev, cudaStream_t
     configured[dev.ordinal] = 1;
   }
   const uint32_t gmax = (uint32_t)std::min(dev.num_sms * max_blocks_per_sm[dev.ordinal], kMaxGrid);
-  uint32_t G = (uint32_t)std::min<uint64_t>(gmax, std::max<uint64_t>(1, ((uint64_t)a.d + kMinPerCta - 1) / kMinPerCta));
+  const uint32_t G =
+      (uint32_t)std::min<uint64_t>(gmax, std::max<uint64_t>(1, ((uint64_t)a.d + kMinPerCta - 1) / kMinPerCta));
   const uint64_t per_unit = ((uint64_t)a.d + (uint64_t)G * 32 - 1) / ((uint64_t)G * 32);
-  a.W = (uint32_t)((per_unit + 7) & ~7ull);
-  const uint64_t total_bytes = (uint64_t)a.d * sizeof(typename Tr::Elem);
-  const uint64_t budget = 64ull << 20;  // keep the prefetched prefix within L2
-  a.prefetch_bytes = (uint32_t)std::min<uint64_t>(
-      total_bytes <= budget ? (uint64_t)a.W * sizeof(typename Tr::Elem) : budget / ((uint64_t)G * 32), 1u << 30);
+  a.W = (uint32_t)((per_unit + 15) & ~15ull);  // 32-byte aligned unit starts for every dtype
+  a.fb = fine_bits<Tr>(a.d);
 
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(G);
@@ -697,7 +964,7 @@ size_t compress_workspace_layout(uint64_t d, int dtype, int gmax, WsLayout* out)
   l.ctrl = off;
   off = up(off + 256);
   l.hist1 = off;
-  off = up(off + (size_t)kFineBins * 4);
+  off = up(off + (size_t)kHistCopies * kFineBinsMax * 4);
   l.hist_lvl = off;
   off = up(off + (size_t)8 * 256 * 4);
   l.cta_a = off;
@@ -707,7 +974,7 @@ size_t compress_workspace_layout(uint64_t d, int dtype, int gmax, WsLayout* out)
   l.fcreg = off;
   off = up(off + (size_t)gmax * kFcCap * key);
   l.lists = off;
-  off = up(off + ((size_t)d + (size_t)gmax * 32 * 8) * entry);
+  off = up(off + ((size_t)d + (size_t)gmax * 32 * 16) * entry);
   l.total = off;
   if (out) *out = l;
   return off;

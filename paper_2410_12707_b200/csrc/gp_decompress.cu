@@ -4,26 +4,30 @@
 //     if k and (indices.min() < 0 or indices.max() >= d): raise IndexOutOfRange
 //     out = np.zeros(d, values.dtype); out[indices] = values
 //
-// Fast path (indices strictly increasing, as topk_compress emits them): one
-// CTA per 4096-element output tile.  Two warps locate the tile's slice of the
-// index array with a 32-ary search, the tile is zero-filled (or, mode 1, loaded
-// for a residual add) in shared memory, the slice is scattered into it, and the
-// tile is written to HBM once with 128-bit stores — every output element is
-// written exactly once.  The same launch validates the index array: each CTA
+// Fast path (indices strictly increasing, as topk_compress emits them): two
+// CTAs per SM, each owning one contiguous output range.  Warps 0/1 locate the
+// range's slice of the index array with a 32-ary search while every warp
+// streams 128-bit zero stores over the range (the search latency hides under
+// the HBM writes); after a CTA barrier the slice is scattered over the zeros,
+// which are still L2-resident, so HBM sees each output line written once.
+// Mode 1 (residual add, not in the reference) skips the zero fill and adds in
+// place.  The same launch validates the index array: each CTA
 // checks a 1/grid share of the k-1 adjacent pairs (strictly increasing) and
 // CTA 0 checks idx[0] >= 0 and idx[k-1] < d; violations are reported in an
 // asynchronous device flag (GP_FLAG_*).
 //
 // General path (unsorted / repeated indices) reproduces numpy's
 // last-write-wins `out[indices] = values` with an atomicMax "winner" pass.
+#include <algorithm>
 #include <type_traits>
 
 #include "gp_kernels.cuh"
 
 namespace gp {
 
-constexpr int kTile = 4096;
-constexpr int kDecThreads = 256;
+constexpr int kDecThreads = 512;
+constexpr int kDecBlocksPerSm = 2;
+constexpr int64_t kMinChunk = 8192;
 
 // ---- value conversions (exact for f32<->f64 widening and bf16<->f32 of bf16 values)
 __device__ __forceinline__ float bf16_to_f32(uint16_t b) { return __uint_as_float((uint32_t)b << 16); }
@@ -63,10 +67,26 @@ __device__ __forceinline__ O add_vals(O a, O b) {
 }
 
 // first j in [0, n) with idx[j] >= target (n if none), computed by one warp.
+// The first round probes 32 positions around `guess` (k*target/d, exact for
+// uniformly spread indices) with a stride of ~sqrt(n)/8, so for top-k payloads
+// the bracket is usually found in one round trip and finished in a second.
 template <class IT>
-__device__ __forceinline__ int64_t warp_lower_bound(const IT* __restrict__ idx, int64_t n, int64_t target) {
+__device__ __forceinline__ int64_t warp_lower_bound(const IT* __restrict__ idx, int64_t n, int64_t target,
+                                                    int64_t guess) {
   const uint32_t lane = threadIdx.x & 31;
   int64_t lo = 0, hi = n;
+  if (n > 32) {
+    const int64_t stride = max((int64_t)1, (int64_t)(sqrtf((float)n) * 0.125f));
+    int64_t p = guess + ((int64_t)lane - 16) * stride;
+    p = p < 0 ? 0 : (p >= n ? n - 1 : p);
+    const bool pred = (int64_t)__ldg(idx + p) < target;
+    const int cnt = __popc(__ballot_sync(kFull, pred));
+    const int64_t below = __shfl_sync(kFull, p, cnt > 0 ? cnt - 1 : 0);
+    const int64_t above = __shfl_sync(kFull, p, cnt < 32 ? cnt : 31);
+    if (cnt > 0) lo = below + 1;
+    if (cnt < 32) hi = above;
+    if (lo > hi) lo = hi;  // only for unsorted input; the pair check flags it
+  }
   while (hi - lo > 32) {
     const int64_t span = hi - lo;
     const int64_t p = lo + (span * (lane + 1)) / 33;
@@ -85,38 +105,36 @@ __device__ __forceinline__ int64_t warp_lower_bound(const IT* __restrict__ idx, 
 template <class IT, class VT, class OT>
 __global__ void __launch_bounds__(kDecThreads) decompress_kernel(const IT* __restrict__ idx,
                                                                  const VT* __restrict__ vals, int64_t k,
-                                                                 int64_t d, OT* __restrict__ out, int mode,
-                                                                 uint32_t* err, int aligned) {
-  __shared__ __align__(16) OT tile[kTile];
+                                                                 int64_t d, int64_t chunk, OT* __restrict__ out,
+                                                                 int mode, uint32_t* err) {
   __shared__ int64_t sh_range[2];
   const uint32_t tid = threadIdx.x, w = tid >> 5, lane = tid & 31;
-  const int64_t t0 = (int64_t)blockIdx.x * kTile;
-  const int64_t t1 = min(t0 + (int64_t)kTile, d);
-  const int n = (int)(t1 - t0);
-  const bool full = aligned && n == kTile;
-
+  const int64_t o0 = min((int64_t)blockIdx.x * chunk, d);
+  const int64_t o1 = min(o0 + chunk, d);
+  // warps 0/1 find this range's slice of the (sorted) index array while every
+  // warp streams zeros over the range; the scatter then overwrites in place.
   if (w < 2) {
-    const int64_t r = warp_lower_bound(idx, k, w == 0 ? t0 : t1);
+    const int64_t t = w == 0 ? o0 : o1;
+    const int64_t r = warp_lower_bound(idx, k, t, d ? (int64_t)(((__int128)k * t) / d) : 0);
     if (lane == 0) sh_range[w] = r;
   }
-  constexpr int kVecs = kTile * (int)sizeof(OT) / 16;
-  uint4* tv = reinterpret_cast<uint4*>(tile);
   if (mode == 0) {
-    for (int i = tid; i < kVecs; i += kDecThreads) tv[i] = make_uint4(0u, 0u, 0u, 0u);
-  } else if (full) {
-    const uint4* ov = reinterpret_cast<const uint4*>(out + t0);
-    for (int i = tid; i < kVecs; i += kDecThreads) tv[i] = ov[i];
-  } else {
-    for (int i = tid; i < n; i += kDecThreads) tile[i] = out[t0 + i];
+    const int64_t n = o1 - o0;
+    const bool vec = ((uintptr_t)(out + o0) % 16) == 0;
+    constexpr int kPer = 16 / (int)sizeof(OT);
+    const int64_t nv = vec ? n / kPer : 0;
+    uint4* ov = reinterpret_cast<uint4*>(out + o0);
+    for (int64_t i = tid; i < nv; i += kDecThreads) ov[i] = make_uint4(0u, 0u, 0u, 0u);
+    for (int64_t i = nv * kPer + tid; i < n; i += kDecThreads) out[o0 + i] = OT(0);
   }
-  __syncthreads();
+  __syncthreads();  // orders the zero stores before the value stores (same CTA, same addresses)
   const int64_t lo = sh_range[0], hi = sh_range[1];
   bool bad = false;
   for (int64_t j = lo + tid; j < hi; j += kDecThreads) {
     const int64_t i = (int64_t)idx[j];
-    if (i >= t0 && i < t1) {
+    if (i >= o0 && i < o1) {
       const OT v = cvt<OT>(vals[j]);
-      tile[i - t0] = mode == 0 ? v : add_vals<OT>(tile[i - t0], v);
+      out[i] = mode == 0 ? v : add_vals<OT>(out[i], v);
     } else {
       bad = true;
     }
@@ -132,12 +150,6 @@ __global__ void __launch_bounds__(kDecThreads) decompress_kernel(const IT* __res
   if (__syncthreads_or(bad) && tid == 0) atomicOr(err, 2u);
   if (blockIdx.x == 0 && tid == 0 && k > 0) {
     if ((int64_t)idx[0] < 0 || (int64_t)idx[k - 1] >= d) atomicOr(err, 1u);
-  }
-  if (full) {
-    uint4* ov = reinterpret_cast<uint4*>(out + t0);
-    for (int i = tid; i < kVecs; i += kDecThreads) ov[i] = tv[i];
-  } else {
-    for (int i = tid; i < n; i += kDecThreads) out[t0 + i] = tile[i];
   }
 }
 
@@ -167,12 +179,14 @@ __global__ void scatter_kernel(const IT* idx, const VT* vals, int64_t k, int64_t
 
 // ---- dispatch
 template <class IT, class VT, class OT>
-static int run_fast(const DecompressArgs& a, cudaStream_t s) {
+static int run_fast(const DecompressArgs& a, const DeviceInfo& dev, cudaStream_t s) {
   if (a.d <= 0) return 0;
-  const int64_t tiles = (a.d + kTile - 1) / kTile;
-  const int aligned = ((uintptr_t)a.out % 16) == 0;
-  decompress_kernel<IT, VT, OT><<<(unsigned)tiles, kDecThreads, 0, s>>>(
-      (const IT*)a.idx, (const VT*)a.vals, a.k, a.d, (OT*)a.out, a.mode, a.err, aligned);
+  const int64_t blocks = std::min<int64_t>((int64_t)dev.num_sms * kDecBlocksPerSm, (a.d + kMinChunk - 1) / kMinChunk);
+  int64_t chunk = (a.d + blocks - 1) / blocks;
+  chunk = (chunk + 1023) & ~(int64_t)1023;  // keeps every range start 4 KiB aligned
+  const int64_t grid = (a.d + chunk - 1) / chunk;
+  decompress_kernel<IT, VT, OT><<<(unsigned)grid, kDecThreads, 0, s>>>(
+      (const IT*)a.idx, (const VT*)a.vals, a.k, a.d, chunk, (OT*)a.out, a.mode, a.err);
   return cudaGetLastError() == cudaSuccess ? 0 : 5;
 }
 
@@ -190,9 +204,9 @@ static int run_general(const DecompressArgs& a, void* scratch, const DeviceInfo&
 template <class IT, class VT>
 static int pick_out(const DecompressArgs& a, void* scratch, const DeviceInfo& dev, cudaStream_t s, bool general) {
   switch (a.out_dtype) {
-    case 0: return general ? run_general<IT, VT, float>(a, scratch, dev, s) : run_fast<IT, VT, float>(a, s);
-    case 1: return general ? run_general<IT, VT, uint16_t>(a, scratch, dev, s) : run_fast<IT, VT, uint16_t>(a, s);
-    case 2: return general ? run_general<IT, VT, double>(a, scratch, dev, s) : run_fast<IT, VT, double>(a, s);
+    case 0: return general ? run_general<IT, VT, float>(a, scratch, dev, s) : run_fast<IT, VT, float>(a, dev, s);
+    case 1: return general ? run_general<IT, VT, uint16_t>(a, scratch, dev, s) : run_fast<IT, VT, uint16_t>(a, dev, s);
+    case 2: return general ? run_general<IT, VT, double>(a, scratch, dev, s) : run_fast<IT, VT, double>(a, dev, s);
     default: return 6;
   }
 }

@@ -12,16 +12,19 @@ constexpr int kCompressThreads = 1024;  // 32 warps; block scans assume exactly 
 constexpr int kMaxGrid = 1024;          // max CTAs of the cooperative compress grid
 constexpr int kMinPerCta = 16384;       // elements per CTA below which the grid shrinks
 constexpr int kCoarseBins = 1 << 12;    // sample histogram (key >> (bits-12))
-constexpr int kFineBins = 1 << 16;      // global candidate histogram (key >> (bits-16))
+constexpr int kFineBitsMax = 20;        // fine candidate histogram: 16..20 bits (grows with d)
+constexpr int kFineBinsMax = 1 << kFineBitsMax;
 constexpr int kWinBins = 8192;          // smem window of the fine histogram
 constexpr int kLowBins = 256;           // smem low window (zeros, NaN, denormals)
-constexpr int kFcCap = 4096;            // final-candidate capacity of the fast path
-constexpr int kSamples = 2048;          // sample size of the watermark estimate
+constexpr int kFcCap = 8192;            // final-candidate capacity of the fast path
 
 // control words at the head of the workspace
-constexpr int kCtrlBarCount = 0;
-constexpr int kCtrlBarGen = 1;
-constexpr int kCtrlMaxBin = 2;
+constexpr int kHistCopies = 8;          // replicas of the fine histogram (CTA c uses c % 8)
+constexpr int kCtrlBar = 0;             // grid-barrier word (top bit flips per barrier)
+constexpr int kCtrlMaxBin = 2;          // 1 + highest fine bin with a candidate
+constexpr int kCtrlMaxLoBin = 3;        // 1 + highest per-CTA watermark bin
+constexpr int kCtrlCands = 4;           // total candidates of stage 1
+constexpr int kCtrlMinLoBin = 5;        // ~(lowest per-CTA watermark bin), via atomicMax
 
 struct CompressArgs {
   const void* x;
@@ -41,8 +44,9 @@ struct CompressArgs {
   void* fcreg;
   void* lists;
   uint32_t W;               // elements per warp unit (multiple of 8), set by the launcher
-  uint32_t prefetch_bytes;  // per-unit L2 prefetch length, set by the launcher
-  int aligned;              // x is 16-byte aligned
+  int aligned;              // x is 32-byte aligned (256-bit row loads)
+  int fb;                   // fine-histogram bits, set by the launcher
+  unsigned long long* dbg;  // optional per-CTA stage timestamps (32 words per CTA)
 };
 
 struct WsLayout {
