@@ -1,0 +1,427 @@
+#!/usr/bin/env python
+"""AdaTopK compress+decompress throughput on B200 (BASELINE.json `metric`).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+Workload (BASELINE.json configs[1]): ResNet-101 batch-64 stage-boundary tensors
+at 224^2 — [64,256,56,56], [64,512,28,28], [64,1024,14,14], [64,2048,7,7] —
+each as an activation (ReLU(N(0,1))) and a gradient (N(0,1)*1e-3), fp32, at
+keep ratios 0.1 / 0.01 / 0.001 (r = 10 / 100 / 1000): 24 compress+decompress
+pairs per step, 771 MB of dense input per step.  Synthetic data, seeded.
+
+One step = every pair through the sm_100a kernels.  At N > 1 (torchrun, one
+process per GPU, NCCL) every rank runs the same workload (weak scaling) and
+the step includes the path's exchange: each rank's compressed frames go to
+rank+1 and the frames from rank-1 are decompressed — the compressed
+stage-boundary send/recv of the north star.  `value` is algorithmic bytes of
+the whole job per second of the slowest rank (CUDA events, max over ranks).
+Algorithmic bytes per pair: compress d*4 + 12k, decompress
+12k + d*4.
+
+`--impl reference` times the reference algorithm on the host (the NumPy port
+in oracle/, the reference being pure Python + NumPy) on a bounded sample of
+the same workload, rank 0 only.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import multiprocessing as mp
+import os
+import statistics
+import subprocess
+import sys
+import time
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+SHAPES = [(64, 256, 56, 56), (64, 512, 28, 28), (64, 1024, 14, 14), (64, 2048, 7, 7)]
+RATIOS = [10.0, 100.0, 1000.0]
+KINDS = ["activation", "gradient"]
+C1_SHAPE = (8, 1024, 768)
+METRIC = "AdaTopK compress+decompress GB/s"
+WORKLOAD = ("configs[1]: ResNet-101 batch-64 stage-boundary activation+gradient compression, "
+            "keep ratios 0.1/0.01/0.001, fp32, 224x224 boundaries")
+
+
+def select_k(d, r):
+    import math
+
+    return max(1, math.floor(d / r))
+
+
+def pair_bytes(d, esz, k):
+    return 2 * (d * esz + 12 * k)
+
+
+def peaks():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        j = json.loads(p.read_text())
+        return float(j.get("hbm_gbs", 6650.0)), "measured"
+    return 6650.0, "fallback"
+
+
+# --------------------------------------------------------------------------- reference arm
+
+
+def _ref_pair(args):
+    shape, kind, ratio, seed = args
+    import numpy as np
+
+    from oracle import compressor_oracle as O
+
+    rng = np.random.default_rng(seed)
+    x = rng.standard_normal(int(np.prod(shape)), dtype=np.float32)
+    x = np.maximum(x, 0) if kind == "activation" else x * np.float32(1e-3)
+    t0 = time.perf_counter()
+    vals, idx, d = O.topk_compress(x, ratio)  # np.argsort(-|x|, kind="stable"), the reference algorithm
+    O.topk_decompress(vals, idx, d)
+    return time.perf_counter() - t0, pair_bytes(d, 4, len(idx))
+
+
+def run_reference(args, rank, world):
+    if rank != 0:
+        return None
+    # bounded sample of the workload: the smallest boundary (act + grad) at all three ratios
+    sample = [(SHAPES[-1], kind, r) for kind in KINDS for r in RATIOS]
+    cores = min(len(sample), os.cpu_count() or 1)
+    times = []
+    with mp.get_context("spawn").Pool(cores) as pool:
+        for step in range(args.warmup + args.steps):
+            t0 = time.perf_counter()
+            res = pool.map(_ref_pair, [(s, k, r, 1000 * step + i) for i, (s, k, r) in enumerate(sample)])
+            dt = time.perf_counter() - t0
+            nbytes = sum(b for _, b in res)
+            if step >= args.warmup:
+                times.append((dt, nbytes))
+    tot_t = sum(t for t, _ in times)
+    tot_b = sum(b for _, b in times)
+    value = tot_b / tot_t / 1e9
+    desc = (f"{len(sample)} pairs/step = [64,2048,7,7] activation+gradient x r=10/100/1000, "
+            f"oracle NumPy port (stable argsort), multiprocessing over {cores} cores")
+    return {
+        "impl": "reference", "metric": METRIC, "value": round(value, 4), "unit": "GB/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(1e3 * tot_t / len(times), 2),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic (seeded ReLU(N(0,1)) activations, N(0,1)*1e-3 gradients)",
+        "config": {"workload": WORKLOAD, "sample": desc},
+        "cpu_baseline": {"value": round(value, 4), "unit": "GB/s", "cores": cores, "kind": "port", "sample": desc},
+        "e2e": {"value": round(value, 4), "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+
+
+# --------------------------------------------------------------------------- GPU arm
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle sampling during the timed region (B200_PROFILING.md)."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index):
+        self.proc = None
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits", "-lms", "20",
+                 "-i", str(gpu_index)], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return None
+        self.proc.terminate()
+        try:
+            out, _ = self.proc.communicate(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+            out, _ = self.proc.communicate()
+        rows = [r.split(",") for r in out.strip().splitlines() if r.count(",") >= 8]
+        if not rows:
+            return None
+        sm = [float(r[1]) for r in rows if r[1].strip().replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in rows if r[2].strip().replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4) if "Active" in r[5 + i] and "Not" not in r[5 + i]})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(rows)}
+
+
+def run_ours(args, rank, world, local_rank):
+    import torch
+    import torch.distributed as dist
+
+    import paper_2410_12707_b200 as P
+    from paper_2410_12707_b200 import _lib
+
+    dev = torch.device("cuda", local_rank)
+    torch.cuda.set_device(dev)
+    L = _lib.lib()
+    peak, peak_kind = peaks()
+
+    # ---- workload, resident in HBM before the timed region
+    g = torch.Generator(device=dev).manual_seed(1234 + rank)
+    units = []
+    for shape in SHAPES:
+        for kind in KINDS:
+            base = torch.randn(shape, device=dev, generator=g)
+            x = torch.relu(base) if kind == "activation" else base * 1e-3
+            x = x.reshape(-1).contiguous()
+            for r in RATIOS:
+                d = x.numel()
+                k = select_k(d, r)
+                units.append({"x": x, "d": d, "k": k, "r": r, "shape": shape, "kind": kind,
+                              "frame": torch.empty(16 + 12 * k, dtype=torch.uint8, device=dev),
+                              "rframe": torch.empty(16 + 12 * k, dtype=torch.uint8, device=dev),
+                              "out": torch.empty(d, device=dev)})
+    dmax = max(u["d"] for u in units)
+    wsb = L.gp_topk_workspace_bytes(dmax, 0)
+    ws = torch.empty(wsb, dtype=torch.uint8, device=dev)
+    err = torch.zeros(1, dtype=torch.int32, device=dev)
+    stream = torch.cuda.current_stream(dev)
+    sp = stream.cuda_stream
+    assert L.gp_workspace_init(ws.data_ptr(), wsb, sp) == 0
+    flush = torch.ones(128 << 20, dtype=torch.float32, device=dev)  # 512 MB read between steps
+    step_bytes = sum(pair_bytes(u["d"], 4, u["k"]) for u in units)
+
+    def compress(u):
+        st = L.gp_topk_compress_frame(u["x"].data_ptr(), 0, u["d"], u["k"], u["frame"].data_ptr(), ws.data_ptr(),
+                                      wsb, sp)
+        assert st == 0, st
+
+    def decompress(u, frame):
+        st = L.gp_topk_decompress_frame(frame.data_ptr(), u["k"], u["d"], u["out"].data_ptr(), 0, 0,
+                                        err.data_ptr(), sp)
+        assert st == 0, st
+
+    def exchange():
+        nxt, prv = (rank + 1) % world, (rank - 1) % world
+        ops = []
+        for u in units:
+            ops.append(dist.P2POp(dist.isend, u["frame"], nxt))
+            ops.append(dist.P2POp(dist.irecv, u["rframe"], prv))
+        for w in dist.batch_isend_irecv(ops):
+            w.wait()
+
+    def step(ev=None):
+        for i, u in enumerate(units):
+            if ev is not None:
+                ev[i][0].record(stream)
+            compress(u)
+            if ev is not None:
+                ev[i][1].record(stream)
+        if world > 1:
+            exchange()
+        for i, u in enumerate(units):
+            if ev is not None:
+                ev[i][2].record(stream)
+            decompress(u, u["rframe"] if world > 1 else u["frame"])
+            if ev is not None:
+                ev[i][3].record(stream)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize(dev)
+
+    # clock sampler first, spun up under load (untimed), then exactly W warm-up steps
+    clocks = ClockSampler(local_rank)
+    t_spin = time.perf_counter()
+    while time.perf_counter() - t_spin < 0.8:
+        step()
+        torch.cuda.synchronize(dev)
+    for _ in range(args.warmup):
+        step()
+    barrier()
+    assert int(err.item()) == 0
+
+    # ---- timed region
+    mk = lambda: torch.cuda.Event(enable_timing=True)  # noqa: E731
+    step_ms, comp_us, decomp_us = [], [], []
+    for _ in range(args.steps):
+        flush.sum()  # L2 flush (outside the events)
+        barrier()
+        s0, s1 = mk(), mk()
+        ev = [[mk() for _ in range(4)] for _ in units]
+        s0.record(stream)
+        step(ev)
+        s1.record(stream)
+        barrier()
+        step_ms.append(s0.elapsed_time(s1))
+        comp_us.append([e[0].elapsed_time(e[1]) * 1e3 for e in ev])
+        decomp_us.append([e[2].elapsed_time(e[3]) * 1e3 for e in ev])
+    clk = clocks.stop()
+    assert int(err.item()) == 0, "decompress validation flag raised"
+
+    t_step = statistics.mean(step_ms)
+    if world > 1:
+        t = torch.tensor([t_step], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        t_step = float(t.item())
+    value = world * step_bytes / (t_step * 1e-3) / 1e9
+
+    # roofline of the dominant kernel (compress): algorithmic bytes / mean launch time
+    comp_bytes = sum(u["d"] * 4 + 12 * u["k"] for u in units)
+    comp_time = sum(sum(c) for c in comp_us) / len(comp_us) * 1e-6
+    decomp_time = sum(sum(c) for c in decomp_us) / len(decomp_us) * 1e-6
+    achieved = comp_bytes / comp_time / 1e9
+    traffic = None
+    tpath = ROOT / "profiles" / "ncu_traffic.json"
+    if tpath.exists():
+        try:
+            traffic = json.loads(tpath.read_text()).get("compress_dram_bytes_per_launch_workload")
+        except (ValueError, OSError):
+            traffic = None
+    per_config = {}
+    for i, u in enumerate(units):
+        key = f"{list(u['shape'])}/{u['kind']}/r={int(u['r'])}"
+        c = statistics.median([cu[i] for cu in comp_us])
+        dd = statistics.median([du[i] for du in decomp_us])
+        per_config[key] = {"compress_us": round(c, 2), "decompress_us": round(dd, 2),
+                           "pair_gbs": round(pair_bytes(u["d"], 4, u["k"]) / ((c + dd) * 1e-6) / 1e9, 1)}
+
+    line = {
+        "metric": METRIC, "value": round(value, 2), "unit": "GB/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": round(t_step, 4), "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic (seeded ReLU(N(0,1)) activations, N(0,1)*1e-3 gradients, per-rank seeds)",
+        "config": {"workload": WORKLOAD, "shapes": [list(s) for s in SHAPES], "ratios": RATIOS,
+                   "pairs_per_step": len(units), "bytes_per_step_per_rank": step_bytes,
+                   "l2": "512 MB read flush between timed steps; each step reads 771 MB of inputs (> L2)",
+                   "parallelism": ("replicas, no exchange" if world == 1 else
+                                   f"{world} ranks, compressed frames ring-exchanged over NCCL P2P (batch_isend_irecv)")},
+        "roofline": {"bound": "hbm", "kernel": "compress_kernel<f32> (cooperative, 1 CTA/SM)",
+                     "achieved": round(achieved, 1), "peak": peak, "peak_kind": peak_kind, "unit": "GB/s",
+                     "frac": round(achieved / peak, 4), "traffic": traffic,
+                     "decompress_achieved": round(comp_bytes / decomp_time / 1e9, 1),
+                     "bytes_per_launch_mean": comp_bytes // len(units)},
+        "per_config": per_config,
+        "gpu_launches": 2 * len(units) * args.steps,
+        "clocks": clk,
+    }
+    if rank == 0 and world == 1:
+        line["c1_gpt2_small"] = bench_c1(P, L, dev, flush, peak)
+        line["cpu_baseline"] = cpu_baseline()
+        line["e2e"] = bench_e2e(P, dev)
+    elif world > 1:
+        line["e2e"] = None
+    return line
+
+
+def bench_c1(P, L, dev, flush, peak, reps=20):
+    """The north-star target config: 8x1024x768 fp32 at r=100, cold L2, CUDA events per launch."""
+    import torch
+
+    g = torch.Generator(device=dev).manual_seed(0)
+    x = torch.randn(C1_SHAPE, device=dev, generator=g).reshape(-1)
+    d = x.numel()
+    k = select_k(d, 100.0)
+    frame = torch.empty(16 + 12 * k, dtype=torch.uint8, device=dev)
+    out = torch.empty(d, device=dev)
+    wsb = L.gp_topk_workspace_bytes(d, 0)
+    ws = torch.empty(wsb, dtype=torch.uint8, device=dev)
+    err = torch.zeros(1, dtype=torch.int32, device=dev)
+    sp = torch.cuda.current_stream(dev).cuda_stream
+    L.gp_workspace_init(ws.data_ptr(), wsb, sp)
+    tc, td = [], []
+    for i in range(reps + 3):
+        flush.sum()
+        e = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+        e[0].record()
+        L.gp_topk_compress_frame(x.data_ptr(), 0, d, k, frame.data_ptr(), ws.data_ptr(), wsb, sp)
+        e[1].record()
+        L.gp_topk_decompress_frame(frame.data_ptr(), k, d, out.data_ptr(), 0, 0, err.data_ptr(), sp)
+        e[2].record()
+        e[2].synchronize()
+        if i >= 3:
+            tc.append(e[0].elapsed_time(e[1]) * 1e3)
+            td.append(e[1].elapsed_time(e[2]) * 1e3)
+    c, dd = statistics.median(tc), statistics.median(td)
+    b = pair_bytes(d, 4, k)
+    return {"shape": list(C1_SHAPE), "ratio": 100, "compress_us": round(c, 2), "decompress_us": round(dd, 2),
+            "pair_us": round(c + dd, 2), "pair_gbs": round(b / ((c + dd) * 1e-6) / 1e9, 1),
+            "frac_of_peak": round(b / ((c + dd) * 1e-6) / 1e9 / peak, 4),
+            "note": "per-launch CUDA events after a 512 MB L2 flush; includes launch latency"}
+
+
+def cpu_baseline():
+    """The reference algorithm (oracle NumPy port) on one [64,2048,7,7] activation at r=100, 1 core."""
+    dt, b = min(_ref_pair((SHAPES[-1], "activation", 100.0, 7)) for _ in range(2))
+    return {"value": round(b / dt / 1e9, 4), "unit": "GB/s", "cores": 1, "kind": "port",
+            "sample": "1 x [64,2048,7,7] fp32 activation, r=100, compress+decompress, best of 2 "
+                      "(np.argsort(kind='stable') is single-threaded)", "cpu_count": os.cpu_count()}
+
+
+def bench_e2e(P, dev, steps=2):
+    """Same workload through the public drop-in API with pinned host inputs and a D2H read of every result."""
+    import torch
+
+    hosts = []
+    g = torch.Generator().manual_seed(99)
+    for shape in SHAPES:
+        for kind in KINDS:
+            base = torch.randn(shape, generator=g)
+            x = (torch.relu(base) if kind == "activation" else base * 1e-3).reshape(-1).contiguous().pin_memory()
+            hosts.append(x)
+    outs = [torch.empty_like(h).pin_memory() for h in hosts]
+    total_bytes, h2d, d2h = 0, 0, 0
+    times = []
+    for s in range(steps + 1):
+        torch.cuda.synchronize(dev)
+        t0 = time.perf_counter()
+        for h, o in zip(hosts, outs):
+            for r in RATIOS:
+                p = P.topk_compress(h, r)          # H2D of the pinned input inside
+                dense = P.topk_decompress(p)       # device result
+                o.copy_(dense)                     # D2H of the result
+                if s == 0:
+                    total_bytes += pair_bytes(h.numel(), 4, p.k)
+                    h2d += h.numel() * 4
+                    d2h += h.numel() * 4
+        torch.cuda.synchronize(dev)
+        if s > 0:
+            times.append(time.perf_counter() - t0)
+    t = statistics.mean(times)
+    return {"value": round(total_bytes / t / 1e9, 2), "unit": "GB/s", "h2d_bytes_per_step": h2d,
+            "d2h_bytes_per_step": d2h, "ms_per_step": round(t * 1e3, 2),
+            "api": "paper_2410_12707_b200.topk_compress / topk_decompress (drop-in for geopipe.compressor)"}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    args = ap.parse_args()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        line = run_reference(args, rank, world)
+        if line is not None:
+            print(json.dumps(line), flush=True)
+        return
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+
+        torch.cuda.set_device(local_rank)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    line = run_ours(args, rank, world, local_rank)
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

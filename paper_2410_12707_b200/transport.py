@@ -1,0 +1,149 @@
+"""Compressed stage-boundary send/recv: the reference executor's message path on GPUs.
+
+The reference delivers every cross-device OpData through an in-process dict
+inbox, compressing on the way (pkg/src/geopipe/executor.py:207-220 and
+:248-297):
+
+    payload, shape = _maybe_compress(value, (src, dst), plan)   # :258 / :281
+    dest.inbox[key] = _maybe_decompress(payload, shape)          # :270-271 / :293
+
+Here the sender GPU compresses straight into the reference wire frame
+(`{d,k} + k*i64 + k*f32`, compressor.py:39-44) with the sm_100a kernel, NCCL
+moves the frame over NVLink (torch.distributed P2P, one process per GPU), and
+the receiver GPU decompresses the frame in place into its activation buffer.
+Both ends size the frame from (d, ratio) alone — k = select_k(d, ratio) is a
+pure function — so no size handshake precedes the payload.
+"""
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass
+from typing import Optional
+
+import torch
+import torch.distributed as dist
+
+from . import _lib
+from .compressor import CompressionPlan, SparsePayload, _DTYPE_CODE, _Workspace, _stream_handle, select_k, \
+    topk_compress, topk_decompress
+from .errors import IndexOutOfRange, raise_for_status
+
+
+def maybe_compress(payload: torch.Tensor, link, plan: Optional[CompressionPlan]):
+    """executor.py:207-214 — pass-through without a plan or at ratio <= 1."""
+    if plan is None:
+        return payload, None
+    ratio = plan.ratio_for(*link)
+    if ratio <= 1.0:
+        return payload, None
+    return topk_compress(payload.reshape(-1), ratio), tuple(payload.shape)
+
+
+def maybe_decompress(payload, shape):
+    """executor.py:217-220."""
+    if shape is None:
+        return payload
+    return topk_decompress(payload).reshape(shape)
+
+
+def frame_bytes(d: int, ratio: float) -> int:
+    return 16 + 12 * select_k(d, ratio)
+
+
+@dataclass
+class FrameCodec:
+    """Device-side compress-to-frame / decompress-from-frame with reusable buffers.
+
+    The hot path of a pipeline stage boundary: no host synchronisation, errors
+    are accumulated in a device flag (`check()` reads it).
+    """
+
+    device: torch.device
+
+    def __post_init__(self):
+        self.err = torch.zeros(1, dtype=torch.int32, device=self.device)
+
+    def compress(self, x: torch.Tensor, ratio: float, frame: Optional[torch.Tensor] = None) -> torch.Tensor:
+        flat = x.reshape(-1)
+        if not flat.is_contiguous():
+            flat = flat.contiguous()
+        d = flat.numel()
+        k = select_k(d, ratio)
+        if frame is None:
+            frame = torch.empty(16 + 12 * k, dtype=torch.uint8, device=self.device)
+        code = _DTYPE_CODE[flat.dtype]
+        sp = _stream_handle(self.device)
+        ws, wsb = _Workspace.get(self.device, sp, d, code)
+        st = _lib.lib().gp_topk_compress_frame(flat.data_ptr(), code, d, k, frame.data_ptr(), ws, wsb, sp)
+        raise_for_status(st, "gp_topk_compress_frame", ratio)
+        return frame
+
+    def decompress(self, frame: torch.Tensor, out: torch.Tensor, ratio: float, accumulate: bool = False):
+        d = out.numel()
+        k = select_k(d, ratio)
+        st = _lib.lib().gp_topk_decompress_frame(frame.data_ptr(), k, d, out.data_ptr(), _DTYPE_CODE[out.dtype],
+                                                 1 if accumulate else 0, self.err.data_ptr(),
+                                                 _stream_handle(self.device))
+        raise_for_status(st, "gp_topk_decompress_frame")
+        return out
+
+    def check(self):
+        flag = int(self.err.item())
+        self.err.zero_()
+        if flag & _lib.FLAG_OUT_OF_RANGE:
+            raise IndexOutOfRange("received frame holds an index outside [0, d)")
+        if flag & _lib.FLAG_UNSORTED:
+            raise ValueError("received frame indices are not strictly increasing")
+
+
+class StageLink:
+    """One directed compressed channel (src rank -> dst rank) of a pipeline.
+
+    `send` compresses on the sender's current stream and posts an NCCL send;
+    `recv` posts the matching receive and decompresses on arrival.  Use
+    `exchange` to group a send and a receive so neighbouring stages cannot
+    deadlock (ncclGroupStart/End via batch_isend_irecv).
+    """
+
+    def __init__(self, device: torch.device, group=None):
+        self.device = device
+        self.group = group
+        self.codec = FrameCodec(device)
+
+    def exchange(self, sends, recvs):
+        """sends: [(tensor, ratio, dst)]; recvs: [(out_tensor, ratio, src)] -> decompressed outs."""
+        ops, frames_in = [], []
+        for x, ratio, dst in sends:
+            if ratio <= 1.0:
+                ops.append(dist.P2POp(dist.isend, x.contiguous(), dst, group=self.group))
+            else:
+                ops.append(dist.P2POp(dist.isend, self.codec.compress(x, ratio), dst, group=self.group))
+        for out, ratio, src in recvs:
+            if ratio <= 1.0:
+                buf = out
+            else:
+                buf = torch.empty(frame_bytes(out.numel(), ratio), dtype=torch.uint8, device=self.device)
+            frames_in.append(buf)
+            ops.append(dist.P2POp(dist.irecv, buf, src, group=self.group))
+        if ops:
+            for w in dist.batch_isend_irecv(ops):
+                w.wait()
+        outs = []
+        for (out, ratio, _src), buf in zip(recvs, frames_in):
+            if ratio > 1.0:
+                self.codec.decompress(buf, out, ratio)
+            outs.append(out)
+        return outs
+
+
+def payload_from_frame(frame: torch.Tensor, values_dtype=torch.float32) -> SparsePayload:
+    """View a device frame as a SparsePayload (float32 values, like the wire)."""
+    d, k = (int(v) for v in frame[:16].view(torch.int64).tolist())
+    idx = frame[16:16 + 8 * k].view(torch.int64)
+    vals = frame[16 + 8 * k:16 + 12 * k].view(torch.float32)
+    if values_dtype != torch.float32:
+        vals = vals.to(values_dtype)
+    return SparsePayload(values=vals, indices=idx, original_len=d, frame=frame)
+
+
+__all__ = ["maybe_compress", "maybe_decompress", "frame_bytes", "FrameCodec", "StageLink", "payload_from_frame"]
