@@ -32,6 +32,7 @@ int device_info(gp::DeviceInfo* info) {
 }
 
 unsigned long long* g_debug_stamps = nullptr;  // development aid, see gp_debug_stamps
+unsigned long long* g_debug_dec = nullptr;     // development aid, see gp_debug_dec_stamps
 
 inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
 
@@ -79,6 +80,7 @@ __global__ void plan_kernel(const double* R, int n, double base, const int64_t* 
 }  // namespace
 
 namespace gp {
+int debug_decompress_occupancy();
 int launch_adatopk_plan(const double* R, int n, double base, const int64_t* dl, double* r_out, int64_t* k_out,
                         int32_t* status, cudaStream_t s) {
   plan_kernel<<<1, 32, 0, s>>>(R, n, base, dl, r_out, k_out, status);
@@ -94,6 +96,8 @@ const char* gp_version(void) { return "adatopk-b200 0.1.0 sm_100a"; }
 // compress launch writes per-CTA stage timestamps (globaltimer ns, clock64)
 // into this device buffer of G*32 u64.
 void gp_debug_stamps(void* dev_buf) { g_debug_stamps = static_cast<unsigned long long*>(dev_buf); }
+void gp_debug_dec_stamps(void* dev_buf) { g_debug_dec = static_cast<unsigned long long*>(dev_buf); }
+int gp_debug_dec_occupancy(void) { return gp::debug_decompress_occupancy(); }
 
 int gp_select_k(int64_t d, double ratio, int64_t* k_out) {
   if (!k_out) return GP_ERR_INVALID_ARGUMENT;
@@ -177,7 +181,7 @@ static int decompress_common(const void* idx, int idx_bytes, const void* vals, i
   if (d == 0 && k > 0) return GP_ERR_INDEX_OUT_OF_RANGE;  // every index is >= d
   gp::DeviceInfo dev;
   if (device_info(&dev)) return GP_ERR_CUDA;
-  gp::DecompressArgs a = {idx, idx_bytes == 8, vals, val_dtype, k, d, out, out_dtype, mode, d_err_flag};
+  gp::DecompressArgs a = {idx, idx_bytes == 8, vals, val_dtype, k, d, out, out_dtype, mode, d_err_flag, g_debug_dec};
   if (scratch) return gp::launch_decompress_unsorted(a, scratch, dev, as_stream(stream));
   return gp::launch_decompress(a, dev, as_stream(stream));
 }

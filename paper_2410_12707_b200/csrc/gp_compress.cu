@@ -48,6 +48,7 @@
 namespace gp {
 
 constexpr int kListBytes = 40 * 1024;  // per-CTA shared-memory candidate lists
+constexpr int kMaxGridSpec = 160;      // largest grid: the one-round-trip FC gather stages G*32 keys in smem
 constexpr int kRowsPerBuf = 2;         // rows per pipeline buffer (x2 buffers in flight)
 
 // ---------------------------------------------------------------------------
@@ -387,7 +388,8 @@ __global__ void __launch_bounds__(kCompressThreads, 1) compress_kernel(const Com
     L = 0;
     uint32_t mymax = 0;
     const Key lo_m1 = lo ? lo - 1 : (Key)0;
-    auto take = [&](uint32_t pos, uint32_t idx, Bits b) {
+    // histogram one candidate (run warp-cooperatively over freshly appended entries)
+    auto count = [&](Bits b) {
       const uint32_t fb = (uint32_t)(Tr::key(b) >> FS);
       if (fb < add_below) {
         const uint32_t off = fb - wb;
@@ -396,20 +398,29 @@ __global__ void __launch_bounds__(kCompressThreads, 1) compress_kernel(const Com
         else atomicAdd(&hist[fb], 1u);
         mymax = max(mymax, fb + 1u);
       }
-      list.put(pos, idx, b);
     };
     // Candidate test in the value domain: one |x| >= thr compare per element
     // (FSETP/DSETP with the abs modifier; NaN compares false, its key is 0).
     const typename Tr::Cand test = Tr::make_cand(lo_m1);
-    auto process = [&](const uint32_t(&buf)[RB][8], uint32_t r0, auto all_tag) {
-      constexpr bool kAll = decltype(all_tag)::value;  // lo == 0: every element, NaN included
+    const bool all = lo == 0;  // every element is a candidate, NaN included
+    // the warp histograms the entries it just appended, one per lane
+    auto count_new = [&](uint32_t from) {
+      __syncwarp();
+      for (uint32_t j = from + lane; j < L; j += 32u) {
+        uint32_t idx;
+        Bits b;
+        list.get(j, idx, b);
+        count(b);
+      }
+    };
+    auto process = [&](const uint32_t(&buf)[RB][8], uint32_t r0) {
       uint32_t m[RB];
 #pragma unroll
       for (int rr = 0; rr < RB; ++rr) {
         uint32_t mm = 0;
 #pragma unroll
         for (int e = 0; e < EPL; ++e)
-          if (kAll || test(chunk_elem<Tr>(buf[rr], e))) mm |= 1u << e;
+          if (all || test(chunk_elem<Tr>(buf[rr], e))) mm |= 1u << e;
         m[rr] = ((r0 + rr) * 32u + lane < nch) ? mm : 0u;
       }
       static_assert(RB == 2, "packed two-row scan");
@@ -418,17 +429,19 @@ __global__ void __launch_bounds__(kCompressThreads, 1) compress_kernel(const Com
         const uint32_t incl = warp_incl_scan(packed);
         const uint32_t excl = incl - packed, tot = __shfl_sync(kFull, incl, 31);
         uint32_t pos[RB] = {L + (excl & 0xFFFFu), L + (tot & 0xFFFFu) + (excl >> 16)};
+        const uint32_t from = L;
         L += (tot & 0xFFFFu) + (tot >> 16);
 #pragma unroll
-        for (int rr = 0; rr < RB; ++rr) {
+        for (int rr = 0; rr < RB; ++rr) {  // divergent part: append only
           uint32_t mm = m[rr];
           const uint32_t base = u0 + ((r0 + rr) * 32u + lane) * EPL;
           while (mm) {
             const uint32_t e = __ffs(mm) - 1;
             mm &= mm - 1;
-            take(pos[rr]++, base + e, chunk_elem<Tr>(buf[rr], e));
+            list.put(pos[rr]++, base + e, chunk_elem<Tr>(buf[rr], e));
           }
         }
+        count_new(from);
       }
     };
     if (!preloaded) {
@@ -436,18 +449,14 @@ __global__ void __launch_bounds__(kCompressThreads, 1) compress_kernel(const Com
       if (nrow > RB) load_rows(nxt, RB);
     }
     // two buffers in flight: while one is being filtered the other is loading
-    auto stream_rows = [&](auto all_tag) {
-      for (uint32_t r0 = 0; r0 < nrow; r0 += 2 * RB) {
-        process(cur, r0, all_tag);
-        if (r0 + 2 * RB < nrow) load_rows(cur, r0 + 2 * RB);
-        if (r0 + RB < nrow) {
-          process(nxt, r0 + RB, all_tag);
-          if (r0 + 3 * RB < nrow) load_rows(nxt, r0 + 3 * RB);
-        }
+    for (uint32_t r0 = 0; r0 < nrow; r0 += 2 * RB) {
+      process(cur, r0);
+      if (r0 + 2 * RB < nrow) load_rows(cur, r0 + 2 * RB);
+      if (r0 + RB < nrow) {
+        process(nxt, r0 + RB);
+        if (r0 + 3 * RB < nrow) load_rows(nxt, r0 + 3 * RB);
       }
-    };
-    if (lo == 0) stream_rows(std::true_type{});
-    else stream_rows(std::false_type{});
+    }
     const Key span = lo ? Tr::kInfAbs - lo_m1 : ~(Key)0;
     for (uint32_t i0 = nch * EPL; i0 < n; i0 += 32u) {  // scalar tail / unaligned input
       const uint32_t i = i0 + lane;
@@ -458,8 +467,10 @@ __global__ void __launch_bounds__(kCompressThreads, 1) compress_kernel(const Com
         f = (Key)(Tr::abs_bits(b) - lo_m1) <= span;
       }
       const uint32_t mk = __ballot_sync(kFull, f);
-      if (f) take(L + __popc(mk & lanemask_lt()), u0 + i, b);
+      const uint32_t from = L;
+      if (f) list.put(L + __popc(mk & lanemask_lt()), u0 + i, b);
       L += __popc(mk);
+      count_new(from);
     }
     mymax = __reduce_max_sync(kFull, mymax);
     if (lane == 0) {
@@ -521,30 +532,29 @@ __global__ void __launch_bounds__(kCompressThreads, 1) compress_kernel(const Com
     return sh_res[0] != 0u;
   };
 
-  stream_unit(lo0, 0xFFFFFFFFu, true);
-  if (tid == 0) {
-    atomicMax(&ctrl[kCtrlMaxLoBin], my_lobin + 1u);
-    atomicMax(&ctrl[kCtrlMinLoBin], 0xFFFFFFFFu - my_lobin);  // min, stored complemented
-  }
-  STAMP(2);
-  grid_barrier(bar, G);  // ---- B1
-  STAMP(3);
+  // first pass, and at most one partial rescan: a CTA whose watermark sat
+  // above B1 (or all of them, if too few candidates overall) re-streams its
+  // chunk with the watermark lowered to B1's edge, adding just the newly
+  // covered bins; B1 can only move up, so one rescan suffices.
   {
-    const bool enough = ctrl[kCtrlCands] >= k;
-    const bool found = enough && find_b1();
-    const uint32_t maxlob = ctrl[kCtrlMaxLoBin] - 1u;
-    if (!found || maxlob > B1) {
-      // Some CTA's watermark sat above B1 (or too few candidates overall):
-      // only those CTAs re-stream their chunk with the watermark lowered to
-      // B1's edge, adding just the newly covered bins; B1 can only move up.
-      const uint32_t b1e = found ? B1 : 0u;
-      if (my_lobin > b1e) {
-        stream_unit((Key)b1e << FS, my_lobin, false);
-        my_lobin = b1e;
-        if (tid == 0) atomicMax(&ctrl[kCtrlMinLoBin], 0xFFFFFFFFu - b1e);
+    Key lo = lo0;
+    uint32_t add_below = 0xFFFFFFFFu;
+    for (int pass = 0;; ++pass) {
+      if (pass == 0 || my_lobin > (uint32_t)(lo >> FS)) {
+        stream_unit(lo, add_below, pass == 0);
+        if (pass == 1) my_lobin = (uint32_t)(lo >> FS);
+        if (tid == 0) {
+          atomicMax(&ctrl[kCtrlMaxLoBin], my_lobin + 1u);
+          atomicMax(&ctrl[kCtrlMinLoBin], 0xFFFFFFFFu - my_lobin);  // min, stored complemented
+        }
       }
-      grid_barrier(bar, G);
-      find_b1();
+      if (pass == 0) STAMP(2);
+      grid_barrier(bar, G);  // ---- B1 (and the rescan barrier)
+      if (pass == 0) STAMP(3);
+      const bool found = (pass == 1 || ctrl[kCtrlCands] >= k) && find_b1();
+      if (pass == 1 || (found && ctrl[kCtrlMaxLoBin] - 1u <= B1)) break;
+      lo = (Key)(found ? B1 : 0u) << FS;
+      add_below = my_lobin;
     }
   }
   STAMP(4);
@@ -583,11 +593,14 @@ __global__ void __launch_bounds__(kCompressThreads, 1) compress_kernel(const Com
   // (except bin 0, which holds both NaN, key 0, and +-0, key 1)
   const bool kDirectT = Tr::kDirectT && B1 != 0;
 
-  if (M <= (uint32_t)kFcCap) {
+  if (M + 2 <= (uint32_t)kFcCap) {
     // ================= fast path =================
+    // Each CTA's FC region: [0] sure count, [1] FC count, [2..] FC keys in
+    // index order, so one coalesced read of 32 words per CTA after B2 returns
+    // every count and (usually) every key.
+    Key* fcreg = reinterpret_cast<Key*>(a.fcreg) + (size_t)c * kFcCap;
     if (!kDirectT) {
-      Key* fcreg = reinterpret_cast<Key*>(a.fcreg) + (size_t)c * kFcCap;
-      uint32_t j0 = w_boff[w];
+      uint32_t j0 = 2 + w_boff[w];
       for (uint32_t base = 0; base < L; base += 32u) {
         const uint32_t j = base + lane;
         bool isfc = false;
@@ -605,28 +618,40 @@ __global__ void __launch_bounds__(kCompressThreads, 1) compress_kernel(const Com
       }
     }
     if (tid == 0) {
-      a.cta_a[c] = sh_res[8];
-      a.cta_b[c] = sh_res[9];
+      fcreg[0] = (Key)sh_res[8];
+      fcreg[1] = (Key)sh_res[9];
     }
     STAMP(5);
     grid_barrier(bar, G);  // ---- B2
     STAMP(6);
 
-    // ---- stage 3: per-CTA prefixes (warp 0), FC list into smem (all warps)
-    uint32_t* tmp_a = sh_fcpre;  // scratch until the FC prefix is built
-    if (tid < G) {               // one global round trip for all per-CTA counts
-      tmp_a[tid] = a.cta_a[tid];
-      sh_fcoff[tid] = a.cta_b[tid];
+    // ---- stage 3: one round trip for every CTA's counts + first kSpec-2 FC keys
+    constexpr uint32_t kSpec = 32;
+    Key* stage = reinterpret_cast<Key*>(smem + SL::coarse);  // coarse + window smem, free after stage 1
+    static_assert(kMaxGridSpec * kSpec * sizeof(Key) <= (kCoarseBins + kWinBins) * 4, "staging fits");
+    {
+      constexpr int R = (kMaxGridSpec * kSpec + kCompressThreads - 1) / kCompressThreads;
+      Key v[R];
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        const uint32_t s = tid + r * kCompressThreads;
+        if (s < G * kSpec) v[r] = reinterpret_cast<const Key*>(a.fcreg)[(size_t)(s / kSpec) * kFcCap + s % kSpec];
+      }
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        const uint32_t s = tid + r * kCompressThreads;
+        if (s < G * kSpec) stage[s] = v[r];
+      }
     }
     __syncthreads();
-    if (w == 0) {
+    if (w == 0) {  // per-CTA prefixes of the sure and FC counts
       const uint32_t per = (G + 31) / 32;
       uint32_t sa = 0, sb = 0;
       for (uint32_t i = 0; i < per; ++i) {
         const uint32_t c2 = lane * per + i;
         if (c2 < G) {
-          sa += tmp_a[c2];
-          sb += sh_fcoff[c2];
+          sa += (uint32_t)stage[c2 * kSpec];
+          sb += (uint32_t)stage[c2 * kSpec + 1];
         }
       }
       const uint32_t ia = warp_incl_scan(sa), ib = warp_incl_scan(sb);
@@ -634,11 +659,10 @@ __global__ void __launch_bounds__(kCompressThreads, 1) compress_kernel(const Com
       for (uint32_t i = 0; i < per; ++i) {
         const uint32_t c2 = lane * per + i;
         if (c2 < G) {
-          const uint32_t va = tmp_a[c2], vb = sh_fcoff[c2];
           if (c2 == c) sh_res[10] = ra;
           sh_fcoff[c2] = rb;
-          ra += va;
-          rb += vb;
+          ra += (uint32_t)stage[c2 * kSpec];
+          rb += (uint32_t)stage[c2 * kSpec + 1];
         }
       }
       if (lane == 31) sh_fcoff[G] = ib;
@@ -651,29 +675,16 @@ __global__ void __launch_bounds__(kCompressThreads, 1) compress_kernel(const Com
     if (kDirectT) {
       T |= 1;  // every FC key equals T; the tie quota is the whole need
     } else {
-      {
-        // gather the index-ordered FC list: position p belongs to the last CTA
-        // whose FC offset is <= p; all loads are issued before any store
-        constexpr int R = kFcCap / kCompressThreads;
-        Key kv[R];
-#pragma unroll
-        for (int r = 0; r < R; ++r) {
-          const uint32_t p = tid + r * kCompressThreads;
-          if (p < Mt) {
-            uint32_t lo = 0, hi = G - 1;
-            while (lo < hi) {
-              const uint32_t mid = (lo + hi + 1) >> 1;
-              if (sh_fcoff[mid] <= p) lo = mid;
-              else hi = mid - 1;
-            }
-            kv[r] = reinterpret_cast<const Key*>(a.fcreg)[(size_t)lo * kFcCap + (p - sh_fcoff[lo])];
-          }
-        }
-#pragma unroll
-        for (int r = 0; r < R; ++r) {
-          const uint32_t p = tid + r * kCompressThreads;
-          if (p < Mt) sh_fckey[p] = kv[r];
-        }
+      // place the index-ordered FC list: staged keys first, then the rest of
+      // any CTA holding more than kSpec-2 (rare second round trip)
+      for (uint32_t s = tid; s < G * kSpec; s += kCompressThreads) {
+        const uint32_t c2 = s / kSpec, j = s % kSpec;
+        if (j >= 2 && j - 2 < (uint32_t)stage[c2 * kSpec + 1]) sh_fckey[sh_fcoff[c2] + j - 2] = stage[s];
+      }
+      for (uint32_t c2 = w; c2 < G; c2 += 32u) {
+        const uint32_t cnt = sh_fcoff[c2 + 1] - sh_fcoff[c2];
+        const Key* src = reinterpret_cast<const Key*>(a.fcreg) + (size_t)c2 * kFcCap + 2;
+        for (uint32_t j = kSpec - 2 + lane; j < cnt; j += 32u) sh_fckey[sh_fcoff[c2] + j] = src[j];
       }
       __syncthreads();
       // in-smem radix select over the low FS bits of the final candidates
@@ -926,7 +937,7 @@ static int launch_compress_t(CompressArgs a, const DeviceInfo& dev, cudaStream_t
     max_blocks_per_sm[dev.ordinal] = nb;
     configured[dev.ordinal] = 1;
   }
-  const uint32_t gmax = (uint32_t)std::min(dev.num_sms * max_blocks_per_sm[dev.ordinal], kMaxGrid);
+  const uint32_t gmax = (uint32_t)std::min(dev.num_sms * max_blocks_per_sm[dev.ordinal], kMaxGridSpec);
   const uint32_t G =
       (uint32_t)std::min<uint64_t>(gmax, std::max<uint64_t>(1, ((uint64_t)a.d + kMinPerCta - 1) / kMinPerCta));
   const uint64_t per_unit = ((uint64_t)a.d + (uint64_t)G * 32 - 1) / ((uint64_t)G * 32);

@@ -6,12 +6,14 @@
 //
 // Fast path (indices strictly increasing, as topk_compress emits them): two
 // CTAs per SM, each owning one contiguous output range.  Warps 0/1 locate the
-// range's slice of the index array with a 32-ary search while every warp
-// streams 128-bit zero stores over the range (the search latency hides under
-// the HBM writes); after a CTA barrier the slice is scattered over the zeros,
-// which are still L2-resident, so HBM sees each output line written once.
-// Mode 1 (residual add, not in the reference) skips the zero fill and adds in
-// place.  The same launch validates the index array: each CTA
+// range's slice of the index array with an interpolation-guided 32-ary search;
+// then the range is produced as 32 KiB tiles built in shared memory (zeros, or
+// for mode 1 — residual add, not in the reference — the current contents),
+// the tile's entries are streamed in coalesced batches and scattered into smem,
+// and the tile is written to HBM once with 128-bit stores: no output line is
+// touched twice (a zero-then-scatter in global memory re-reads every line a
+// value lands in once the output exceeds L2).  The same launch validates the
+// index array: each CTA
 // checks a 1/grid share of the k-1 adjacent pairs (strictly increasing) and
 // CTA 0 checks idx[0] >= 0 and idx[k-1] < d; violations are reported in an
 // asynchronous device flag (GP_FLAG_*).
@@ -26,7 +28,8 @@
 namespace gp {
 
 constexpr int kDecThreads = 512;
-constexpr int kDecBlocksPerSm = 2;
+constexpr int kDecBlocksPerSm = 4;
+constexpr int kTileBytes = 16 * 1024;   // smem output tile (double-buffered)
 constexpr int64_t kMinChunk = 8192;
 
 // ---- value conversions (exact for f32<->f64 widening and bf16<->f32 of bf16 values)
@@ -103,54 +106,146 @@ __device__ __forceinline__ int64_t warp_lower_bound(const IT* __restrict__ idx, 
 }
 
 template <class IT, class VT, class OT>
-__global__ void __launch_bounds__(kDecThreads) decompress_kernel(const IT* __restrict__ idx,
-                                                                 const VT* __restrict__ vals, int64_t k,
-                                                                 int64_t d, int64_t chunk, OT* __restrict__ out,
-                                                                 int mode, uint32_t* err) {
-  __shared__ int64_t sh_range[2];
-  const uint32_t tid = threadIdx.x, w = tid >> 5, lane = tid & 31;
+__global__ void __launch_bounds__(kDecThreads, kDecBlocksPerSm) decompress_kernel(
+    const IT* __restrict__ idx, const VT* __restrict__ vals, int64_t k, int64_t d, int64_t chunk,
+    OT* __restrict__ out, int mode, uint32_t* err, unsigned long long* dbg) {
+  constexpr int kTileElems = kTileBytes / (int)sizeof(OT);
+  constexpr int kVecs = kTileBytes / 16;
+#define DSTAMP(i)                                                \
+  do {                                                           \
+    if (dbg != nullptr && threadIdx.x == 0) {                    \
+      unsigned long long t_;                                     \
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));     \
+      dbg[(size_t)blockIdx.x * 8 + (i)] = t_;                    \
+    }                                                            \
+  } while (0)
+  DSTAMP(0);
+  __shared__ __align__(16) OT tiles[2][kTileElems];
+  __shared__ int64_t sh_lo;
+  const uint32_t tid = threadIdx.x, lane = tid & 31;
   const int64_t o0 = min((int64_t)blockIdx.x * chunk, d);
   const int64_t o1 = min(o0 + chunk, d);
-  // warps 0/1 find this range's slice of the (sorted) index array while every
-  // warp streams zeros over the range; the scatter then overwrites in place.
-  if (w < 2) {
-    const int64_t t = w == 0 ? o0 : o1;
-    const int64_t r = warp_lower_bound(idx, k, t, d ? (int64_t)(((__int128)k * t) / d) : 0);
-    if (lane == 0) sh_range[w] = r;
-  }
-  if (mode == 0) {
-    const int64_t n = o1 - o0;
-    const bool vec = ((uintptr_t)(out + o0) % 16) == 0;
-    constexpr int kPer = 16 / (int)sizeof(OT);
-    const int64_t nv = vec ? n / kPer : 0;
-    uint4* ov = reinterpret_cast<uint4*>(out + o0);
-    for (int64_t i = tid; i < nv; i += kDecThreads) ov[i] = make_uint4(0u, 0u, 0u, 0u);
-    for (int64_t i = nv * kPer + tid; i < n; i += kDecThreads) out[o0 + i] = OT(0);
-  }
-  __syncthreads();  // orders the zero stores before the value stores (same CTA, same addresses)
-  const int64_t lo = sh_range[0], hi = sh_range[1];
   bool bad = false;
-  for (int64_t j = lo + tid; j < hi; j += kDecThreads) {
-    const int64_t i = (int64_t)idx[j];
-    if (i >= o0 && i < o1) {
-      const OT v = cvt<OT>(vals[j]);
-      out[i] = mode == 0 ? v : add_vals<OT>(out[i], v);
+  // This CTA's 1/grid share of the k-1 adjacent-pair checks (covers every
+  // pair whatever the input); the first pair per thread is loaded now and
+  // compared at the end, so its latency overlaps the rest.
+  const int64_t P = k > 1 ? k - 1 : 0;
+  const int64_t pb = (P * (int64_t)blockIdx.x) / gridDim.x;
+  const int64_t pe = (P * ((int64_t)blockIdx.x + 1)) / gridDim.x;
+  int64_t pa = 0, pz = 1;
+  if (pb + tid < pe) {
+    pa = (int64_t)__ldg(idx + pb + tid);
+    pz = (int64_t)__ldg(idx + pb + tid + 1);
+  }
+  int64_t first = 0, last = 0;
+  if (blockIdx.x == 0 && tid == 0 && k > 0) {
+    first = (int64_t)__ldg(idx);
+    last = (int64_t)__ldg(idx + k - 1);
+  }
+  // Entries are consumed in index order through a register window of one
+  // entry per thread (batch of kDecThreads) with the next batch prefetched.
+  // The first batch is loaded around the interpolation guess k*o0/d, so for
+  // well-spread indices the start of this CTA's entries is found inside it
+  // (a block count) with no separate search round trip.
+  int64_t ci = 0, ni = 0;
+  VT cv = VT(0), nv = VT(0);
+  auto fetch = [&](int64_t b, int64_t& i, VT& v) {
+    const int64_t j = b + tid;
+    if (j >= 0 && j < k) {
+      i = (int64_t)__ldg(idx + j);
+      v = __ldg(vals + j);
+      return true;
+    }
+    return false;
+  };
+  // Round trip 1: all threads probe the index array around the interpolation
+  // guess k*o0/d with a stride covering +-3 sigma of a uniform spread, which
+  // brackets lower_bound(o0) to within one stride (< one batch).  Round trip
+  // 2 loads the batch starting at the bracket.  Clustered indices that the
+  // probe window misses fall back to a 32-ary search.
+  const int64_t guess = d ? (int64_t)((double)k * (double)o0 / (double)d) : 0;  // a guess; rounding is harmless
+  const int64_t stride = max((int64_t)1, (int64_t)(3.0f * sqrtf((float)k) / kDecThreads) + 1);
+  auto probe_pos = [&](int64_t t) {
+    const int64_t p = guess + (t - kDecThreads / 2) * stride;
+    return p < 0 ? (int64_t)0 : (p >= k ? k - 1 : p);
+  };
+  int64_t base = 0;
+  if (k > 0) {
+    const int64_t p = probe_pos(tid);
+    const int64_t pv = (int64_t)__ldg(idx + p);
+    // consume the early loads here (not at the end, where the compiler would
+    // otherwise sink them into an extra serialized round trip)
+    if (!(pa < pz)) bad = true;
+    if (blockIdx.x == 0 && tid == 0 && (first < 0 || last >= d)) atomicOr(err, 1u);
+    const int below = __syncthreads_count(pv < o0);
+    const int64_t p_first = probe_pos(0), p_last = probe_pos(kDecThreads - 1);
+    if ((below == 0 && p_first > 0) || (below == kDecThreads && p_last < k - 1)) {
+      if (tid < 32) {  // probe window missed (clustered indices)
+        const int64_t r = warp_lower_bound(idx, k, o0, guess);
+        if (lane == 0) sh_lo = r;
+      }
+      __syncthreads();
+      base = sh_lo;
     } else {
-      bad = true;
+      base = below == 0 ? 0 : probe_pos(below - 1) + 1;  // lower_bound(o0) in [base, base + stride]
     }
   }
-  // validation share: pairs [pb, pe) must be strictly increasing
-  if (k > 1) {
-    const int64_t P = k - 1;
-    const int64_t pb = (P * (int64_t)blockIdx.x) / gridDim.x;
-    const int64_t pe = (P * ((int64_t)blockIdx.x + 1)) / gridDim.x;
-    for (int64_t j = pb + tid; j < pe; j += kDecThreads)
-      if (!((int64_t)idx[j] < (int64_t)idx[j + 1])) bad = true;
+  const bool have = fetch(base, ci, cv);
+  bool nhave = fetch(base + kDecThreads, ni, nv);
+  bool pend = have && ci >= o0;  // entries below o0 belong to earlier CTAs
+  DSTAMP(1);
+  const bool vec_ok = ((uintptr_t)out % 16) == 0;
+  int par = 0;
+  DSTAMP(2);
+  // Output tiles are built in shared memory (zeros or, mode 1, the current
+  // contents), the tile's entries are scattered into smem, and the tile is
+  // written once with 128-bit stores: every output line reaches HBM once.
+  for (int64_t t0 = o0; t0 < o1; t0 += kTileElems, par ^= 1) {
+    OT* tile = tiles[par];
+    const int n = (int)min((int64_t)kTileElems, o1 - t0);
+    const bool full = vec_ok && n == kTileElems;
+    uint4* tv = reinterpret_cast<uint4*>(tile);
+    if (mode == 0) {
+      for (int i = tid; i < kVecs; i += kDecThreads) tv[i] = make_uint4(0u, 0u, 0u, 0u);
+    } else if (full) {
+      const uint4* ov = reinterpret_cast<const uint4*>(out + t0);
+      for (int i = tid; i < kVecs; i += kDecThreads) tv[i] = ov[i];
+    } else {
+      for (int i = tid; i < n; i += kDecThreads) tile[i] = out[t0 + i];
+    }
+    __syncthreads();
+    const int64_t t1 = t0 + n;
+    for (;;) {
+      if (pend && ci < t1) {
+        if (ci >= t0) {
+          const OT v = cvt<OT>(cv);
+          tile[ci - t0] = mode == 0 ? v : add_vals<OT>(tile[ci - t0], v);
+        } else {
+          bad = true;  // below the tile: only possible for unsorted input
+        }
+        pend = false;
+      }
+      // barrier + "is the whole batch consumed?" (sorted input consumes prefixes)
+      if (__syncthreads_count(pend) != 0 || base + kDecThreads >= k) break;
+      base += kDecThreads;
+      ci = ni;
+      cv = nv;
+      pend = nhave;
+      nhave = fetch(base + kDecThreads, ni, nv);
+    }
+    if (full) {
+      uint4* ov = reinterpret_cast<uint4*>(out + t0);
+      for (int i = tid; i < kVecs; i += kDecThreads) ov[i] = tv[i];
+    } else {
+      for (int i = tid; i < n; i += kDecThreads) out[t0 + i] = tile[i];
+    }
   }
+  DSTAMP(3);
+  for (int64_t j = pb + tid + kDecThreads; j < pe; j += kDecThreads)
+    if (!((int64_t)__ldg(idx + j) < (int64_t)__ldg(idx + j + 1))) bad = true;
   if (__syncthreads_or(bad) && tid == 0) atomicOr(err, 2u);
-  if (blockIdx.x == 0 && tid == 0 && k > 0) {
-    if ((int64_t)idx[0] < 0 || (int64_t)idx[k - 1] >= d) atomicOr(err, 1u);
-  }
+  DSTAMP(4);
+#undef DSTAMP
 }
 
 // ---- general path
@@ -183,10 +278,17 @@ static int run_fast(const DecompressArgs& a, const DeviceInfo& dev, cudaStream_t
   if (a.d <= 0) return 0;
   const int64_t blocks = std::min<int64_t>((int64_t)dev.num_sms * kDecBlocksPerSm, (a.d + kMinChunk - 1) / kMinChunk);
   int64_t chunk = (a.d + blocks - 1) / blocks;
-  chunk = (chunk + 1023) & ~(int64_t)1023;  // keeps every range start 4 KiB aligned
+  const int64_t tile_elems = kTileBytes / (int64_t)sizeof(OT);
+  chunk = (chunk + tile_elems - 1) / tile_elems * tile_elems;  // whole, 16-byte aligned tiles
   const int64_t grid = (a.d + chunk - 1) / chunk;
+  static bool carveout_set[64] = {false};  // 4 CTAs x 32 KiB per SM needs the max-shared carveout
+  if (!carveout_set[dev.ordinal]) {
+    cudaFuncSetAttribute(decompress_kernel<IT, VT, OT>, cudaFuncAttributePreferredSharedMemoryCarveout,
+                         cudaSharedmemCarveoutMaxShared);
+    carveout_set[dev.ordinal] = true;
+  }
   decompress_kernel<IT, VT, OT><<<(unsigned)grid, kDecThreads, 0, s>>>(
-      (const IT*)a.idx, (const VT*)a.vals, a.k, a.d, chunk, (OT*)a.out, a.mode, a.err);
+      (const IT*)a.idx, (const VT*)a.vals, a.k, a.d, chunk, (OT*)a.out, a.mode, a.err, a.dbg);
   return cudaGetLastError() == cudaSuccess ? 0 : 5;
 }
 
@@ -229,4 +331,17 @@ int launch_decompress_unsorted(const DecompressArgs& a, void* scratch, const Dev
   return a.idx64 ? pick_val<int64_t>(a, scratch, dev, s, true) : pick_val<int32_t>(a, scratch, dev, s, true);
 }
 
+}  // namespace gp
+
+namespace gp {
+// development aid: resident CTAs per SM of the fast decompress kernel (f32, i64 indices)
+int debug_decompress_occupancy() {
+  int nb = -1;
+  cudaFuncSetAttribute(decompress_kernel<int64_t, float, float>, cudaFuncAttributePreferredSharedMemoryCarveout,
+                       cudaSharedmemCarveoutMaxShared);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, decompress_kernel<int64_t, float, float>, kDecThreads, 0);
+  cudaFuncAttributes fa;
+  cudaFuncGetAttributes(&fa, decompress_kernel<int64_t, float, float>);
+  return nb * 1000000 + fa.numRegs * 1000 + (int)(fa.sharedSizeBytes / 1024);
+}
 }  // namespace gp

@@ -72,6 +72,7 @@ struct DecompressArgs {
   int out_dtype;
   int mode;
   uint32_t* err;
+  unsigned long long* dbg;  // optional per-CTA stage timestamps (8 words per CTA)
 };
 
 int launch_decompress(const DecompressArgs& a, const DeviceInfo& dev, cudaStream_t stream);

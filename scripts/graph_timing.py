@@ -91,10 +91,12 @@ def main():
             t1 = graph_time([fl, comp])
             t2 = graph_time([fl, comp, decomp])
             tw = graph_time([comp])
+            twd = graph_time([decomp])
+            tsl = graph_time([fl, lambda: torch.cuda._sleep(1)]) - t0
             tc, td = t1 - t0, t2 - t1
             cb = d * esz + 12 * k
             print(f"{name:26s} r={r:6g} k={k:8d} | compress {tc:7.2f} us {cb / tc / 1e3:6.0f} GB/s"
-                  f" (warm {tw:6.2f}) | decompress {td:7.2f} us {cb / td / 1e3:6.0f} GB/s | pair {tc + td:7.2f} us"
+                  f" (warm {tw:6.2f}) | decompress {td:7.2f} us {cb / td / 1e3:6.0f} GB/s (warm {twd:6.2f}) | cold tiny kernel {tsl:5.2f} | pair {tc + td:7.2f} us"
                   f" = {2 * cb / (tc + td) / 1e3 / peak * 100:5.1f}% of {peak:.0f} GB/s", flush=True)
             for label in ("cold", "warm"):
                 if label == "cold":

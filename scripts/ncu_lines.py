@@ -66,12 +66,13 @@ def main():
     ap.add_argument("report")
     ap.add_argument("kernel")
     ap.add_argument("--top", type=int, default=40)
+    ap.add_argument("--fn", default=None, help="substring of the mangled function name (disambiguates templates)")
     args = ap.parse_args()
     tables = line_table(args.kernel)
     for k in ncu_sass(args.report, args.kernel):
         hdr = k["hdr"]
         stalls = [h for h in hdr if h.startswith("stall_") and "Not Issued" not in h]
-        cands = [fn for fn in tables if re.search(args.kernel.lstrip("^"), fn)]
+        cands = [fn for fn in tables if re.search(args.kernel.lstrip("^"), fn) and (args.fn is None or args.fn in fn)]
         # pick the function whose instruction count matches
         fn = next((f for f in cands if len(tables[f]) == len(k["rows"])), cands[0] if cands else None)
         tab = tables.get(fn, {})
@@ -85,6 +86,10 @@ def main():
             total += s
             loc = tab.get(i) or ("?", 0)
             agg[loc]["_all"] += s
+            try:
+                agg[loc]["_inst"] += float(r[hdr["Instructions Executed"]] or 0)
+            except (ValueError, KeyError):
+                pass
             for st in stalls:
                 try:
                     agg[loc][st[6:]] += float(r[hdr[st]] or 0)
@@ -92,8 +97,9 @@ def main():
                     pass
         print(f"== {k['name'][:100]}  ({fn}, {len(k['rows'])} instr, {total:.0f} samples)")
         for loc, d in sorted(agg.items(), key=lambda kv: -kv[1]["_all"])[: args.top]:
-            top = sorted(((s, v) for s, v in d.items() if s != "_all"), key=lambda kv: -kv[1])[:3]
-            print(f"  {loc[0]}:{loc[1]:<5d} {d['_all']:6.0f} ({100 * d['_all'] / max(total, 1):4.1f}%)  "
+            top = sorted(((s, v) for s, v in d.items() if not s.startswith("_")), key=lambda kv: -kv[1])[:3]
+            print(f"  {loc[0]}:{loc[1]:<5d} {d['_all']:6.0f} ({100 * d['_all'] / max(total, 1):4.1f}%) "
+                  f"inst {d['_inst'] / 1e3:8.1f}K  "
                   + ", ".join(f"{s}={v:.0f}" for s, v in top if v))
 
 
