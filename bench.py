@@ -408,6 +408,7 @@ def main():
             print(json.dumps(line), flush=True)
         return
     if world > 1:
+        os.environ.setdefault("NCCL_DEBUG", "WARN")  # keep stdout to the one JSON line
         import torch
         import torch.distributed as dist
 

@@ -16,7 +16,6 @@ pure function — so no size handshake precedes the payload.
 """
 from __future__ import annotations
 
-import math
 from dataclasses import dataclass
 from typing import Optional
 
@@ -97,18 +96,20 @@ class FrameCodec:
 
 
 class StageLink:
-    """One directed compressed channel (src rank -> dst rank) of a pipeline.
+    """Compressed channels between pipeline ranks (one process per GPU).
 
-    `send` compresses on the sender's current stream and posts an NCCL send;
-    `recv` posts the matching receive and decompresses on arrival.  Use
-    `exchange` to group a send and a receive so neighbouring stages cannot
-    deadlock (ncclGroupStart/End via batch_isend_irecv).
+    `exchange` compresses every outgoing tensor into a reference wire frame on
+    the sender's current stream, posts all sends and receives as one NCCL
+    group (`batch_isend_irecv`, so neighbouring stages cannot deadlock),
+    waits, and decompresses every received frame into its destination buffer.
+    The codec is pluggable (default: the sm_100a `FrameCodec`); frame sizes are
+    derived from (d, ratio) on both ends.
     """
 
-    def __init__(self, device: torch.device, group=None):
+    def __init__(self, device: torch.device, group=None, codec=None):
         self.device = device
         self.group = group
-        self.codec = FrameCodec(device)
+        self.codec = codec if codec is not None else FrameCodec(device)
 
     def exchange(self, sends, recvs):
         """sends: [(tensor, ratio, dst)]; recvs: [(out_tensor, ratio, src)] -> decompressed outs."""
@@ -122,7 +123,7 @@ class StageLink:
             if ratio <= 1.0:
                 buf = out
             else:
-                buf = torch.empty(frame_bytes(out.numel(), ratio), dtype=torch.uint8, device=self.device)
+                buf = torch.empty(frame_bytes(out.numel(), ratio), dtype=torch.uint8, device=out.device)
             frames_in.append(buf)
             ops.append(dist.P2POp(dist.irecv, buf, src, group=self.group))
         if ops:

@@ -1,0 +1,120 @@
+"""Multi-rank message path (executor.py:207-297 restated over torch.distributed).
+
+CPU: world_size-2 gloo processes exchange reference wire frames through
+StageLink with an oracle codec — checks the protocol (frame sizing from
+(d, ratio) alone, grouped send/recv in a ring, pass-through at ratio <= 1).
+GPU (-m gpu, >= 2 devices): the same exchange over NCCL with the sm_100a codec,
+checked bit-exactly against the oracle.
+"""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as tmp
+
+from oracle import compressor_oracle as O
+from paper_2410_12707_b200 import transport as T
+from paper_2410_12707_b200.compressor import CompressionPlan
+
+
+class OracleCodec:
+    """CPU codec producing the reference frame with the oracle (test only)."""
+
+    def compress(self, x, ratio):
+        return torch.frombuffer(bytearray(O.compress_frame(x.reshape(-1).numpy(), ratio)), dtype=torch.uint8)
+
+    def decompress(self, frame, out, ratio):
+        vals, idx, d = O.from_bytes(frame.numpy().tobytes())
+        out.reshape(-1).copy_(torch.from_numpy(O.topk_decompress(vals.astype(np.float32), idx, d)))
+        return out
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _inputs(rank, shapes):
+    g = torch.Generator().manual_seed(100 + rank)
+    return [torch.randn(s, generator=g) for s in shapes]
+
+
+SHAPES = [(4, 33, 7), (1000,), (3, 512)]
+RATIOS = [10.0, 1.0, 97.0]
+
+
+def _ring_worker(rank, world, port, backend, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    try:
+        if backend == "nccl":
+            torch.cuda.set_device(rank)
+            dist.init_process_group("nccl", rank=rank, world_size=world, device_id=torch.device("cuda", rank))
+            dev = torch.device("cuda", rank)
+            link = T.StageLink(dev)
+        else:
+            dist.init_process_group("gloo", rank=rank, world_size=world)
+            dev = torch.device("cpu")
+            link = T.StageLink(dev, codec=OracleCodec())
+        xs = [x.to(dev) for x in _inputs(rank, SHAPES)]
+        outs = [torch.empty(s, device=dev) for s in SHAPES]
+        nxt, prv = (rank + 1) % world, (rank - 1) % world
+        got = link.exchange([(x, r, nxt) for x, r in zip(xs, RATIOS)],
+                            [(o, r, prv) for o, r in zip(outs, RATIOS)])
+        # expected: the oracle applied to the previous rank's inputs
+        src = _inputs(prv, SHAPES)
+        ok = True
+        for x, o, r in zip(src, got, RATIOS):
+            flat = x.reshape(-1).numpy()
+            if r <= 1.0:
+                exp = flat
+            else:
+                vals, idx, d = O.topk_compress(flat, r)
+                exp = O.topk_decompress(vals, idx, d)
+            ok &= np.array_equal(o.reshape(-1).cpu().numpy().view(np.uint32), exp.view(np.uint32))
+        dist.barrier()
+        dist.destroy_process_group()
+        q.put((rank, bool(ok)))
+    except Exception as e:  # surface failures to the parent
+        q.put((rank, repr(e)))
+
+
+def _run(world, backend):
+    ctx = tmp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    ps = [ctx.Process(target=_ring_worker, args=(r, world, port, backend, q)) for r in range(world)]
+    for p in ps:
+        p.start()
+    res = dict(q.get(timeout=300) for _ in range(world))
+    for p in ps:
+        p.join(timeout=60)
+    return res
+
+
+def test_ring_exchange_gloo_world2():
+    res = _run(2, "gloo")
+    assert res == {0: True, 1: True}, res
+
+
+def test_frame_bytes_and_passthrough():
+    assert T.frame_bytes(100, 100) == 16 + 12
+    assert T.frame_bytes(6291456, 100) == 16 + 12 * 62914
+    x = torch.randn(3, 4)
+    payload, shape = T.maybe_compress(x, ("a", "b"), None)
+    assert payload is x and shape is None
+    plan = CompressionPlan(base_ratio=10, per_link={("a", "b"): 10.0})
+    payload, shape = T.maybe_compress(x, ("b", "a"), plan)  # link not in plan -> ratio 1.0
+    assert payload is x and shape is None
+    assert T.maybe_decompress(x, None) is x
+
+
+@pytest.mark.gpu
+def test_ring_exchange_nccl_world2(cuda):
+    if torch.cuda.device_count() < 2:
+        pytest.skip("needs 2 GPUs (run under gpurun --gpus 2)")
+    res = _run(2, "nccl")
+    assert res == {0: True, 1: True}, res
