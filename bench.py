@@ -231,10 +231,17 @@ def run_ours(args, rank, world, local_rank):
 
     # clock sampler first, spun up under load (untimed), then exactly W warm-up steps
     clocks = ClockSampler(local_rank)
-    t_spin = time.perf_counter()
-    while time.perf_counter() - t_spin < 0.8:
+    # a fixed, rank-agreed number of spin-up steps (~0.8 s): every rank must run
+    # the same number of exchanges or the NCCL P2P pairing breaks
+    t_one = time.perf_counter()
+    step()
+    torch.cuda.synchronize(dev)
+    t_one = torch.tensor([time.perf_counter() - t_one], device=dev)
+    if world > 1:
+        dist.all_reduce(t_one, op=dist.ReduceOp.MAX)
+    for _ in range(max(1, min(400, int(0.8 / max(float(t_one.item()), 1e-4))))):
         step()
-        torch.cuda.synchronize(dev)
+    torch.cuda.synchronize(dev)
     for _ in range(args.warmup):
         step()
     barrier()
@@ -309,8 +316,59 @@ def run_ours(args, rank, world, local_rank):
         line["cpu_baseline"] = cpu_baseline()
         line["e2e"] = bench_e2e(P, dev)
     elif world > 1:
-        line["e2e"] = None
+        line["e2e"] = bench_e2e_dist(P, dev, rank, world)
+    # the GPT-2 pipeline half of the BASELINE metric: GPT-2 medium, one stage
+    # per GPU, AdaTopK r=100 on every FP/BP boundary (configs[2]; N=1 = no boundary)
+    del units, ws, flush
+    torch.cuda.empty_cache()
+    if not args.no_pipeline:
+        from paper_2410_12707_b200 import pipeline as PL
+
+        line["pipeline"] = PL.run_pipeline("medium", "uniform", 100.0, n_micro=8, steps=3, warmup=2)
+        if world == 8:  # configs[3]: GPT-2 XL, 8 stages, Eq. 6 ratios from a two-cluster link model
+            line["pipeline_xl_adatopk"] = PL.run_pipeline("xl", "adatopk", 100.0, steps=2, warmup=1)
     return line
+
+
+def bench_e2e_dist(P, dev, rank, world, steps=2):
+    """Public API end to end at N ranks: pinned host input -> compress -> NCCL frame exchange -> decompress -> D2H."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2410_12707_b200 import transport as T
+
+    link = T.StageLink(dev)
+    g = torch.Generator().manual_seed(99 + rank)
+    hosts = []
+    for shape in SHAPES:
+        for kind in KINDS:
+            base = torch.randn(shape, generator=g)
+            hosts.append((torch.relu(base) if kind == "activation" else base * 1e-3).reshape(-1).contiguous().pin_memory())
+    outs = [torch.empty_like(h).pin_memory() for h in hosts]
+    bufs = [torch.empty(h.numel(), device=dev) for h in hosts]
+    nxt, prv = (rank + 1) % world, (rank - 1) % world
+    total_bytes = sum(pair_bytes(h.numel(), 4, select_k(h.numel(), r)) for h in hosts for r in RATIOS)
+    h2d = d2h = sum(h.numel() * 4 for h in hosts) * len(RATIOS)
+    times = []
+    for s in range(steps + 1):
+        dist.barrier()
+        torch.cuda.synchronize(dev)
+        t0 = time.perf_counter()
+        for r in RATIOS:
+            xs = [h.to(dev, non_blocking=True) for h in hosts]
+            link.exchange([(x, r, nxt) for x in xs], [(b, r, prv) for b in bufs])
+            for b, o in zip(bufs, outs):
+                o.copy_(b)
+        torch.cuda.synchronize(dev)
+        dt = time.perf_counter() - t0
+        tt = torch.tensor([dt], device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        if s > 0:
+            times.append(float(tt.item()))
+    t = statistics.mean(times)
+    return {"value": round(world * total_bytes / t / 1e9, 2), "unit": "GB/s", "h2d_bytes_per_step": h2d,
+            "d2h_bytes_per_step": d2h, "ms_per_step": round(t * 1e3, 2),
+            "api": "transport.StageLink.exchange (compress -> NCCL P2P -> decompress) on pinned host buffers"}
 
 
 def bench_c1(P, L, dev, flush, peak, reps=20):
@@ -398,6 +456,7 @@ def main():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-pipeline", action="store_true", help="skip the GPT-2 pipeline sub-measurement")
     args = ap.parse_args()
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -413,7 +472,9 @@ def main():
         import torch.distributed as dist
 
         torch.cuda.set_device(local_rank)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        from datetime import timedelta
+
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank), timeout=timedelta(seconds=120))
     line = run_ours(args, rank, world, local_rank)
     if rank == 0:
         print(json.dumps(line), flush=True)

@@ -1,0 +1,350 @@
+"""GPT-2 pipeline training with AdaTopK-compressed stage boundaries.
+
+The reference runs a GPipe fill-drain iteration on in-process workers
+(pkg/src/geopipe/executor.py:376-411): every micro-batch forward, then every
+micro-batch backward, messages compressed per cross-device link
+(`_send_activation` :248-274, `_send_gradient` :276-297), then SGD.  Here each
+stage is one GPU process (torch.distributed, NCCL); activations go forward and
+gradients go backward as AdaTopK wire frames produced by the sm_100a kernels
+(`transport.FrameCodec`), with per-link ratios from `adatopk_plan` (Eq. 6) or
+`uniform_plan`.  Stage compute is plain PyTorch (bf16 autocast matmuls, fp32
+residual stream, so boundary tensors are fp32).
+
+The partition is contiguous and equal in layers — what OP-Fence's
+proportional split (opfence.py:412-424) yields for a homogeneous chain of
+identical blocks.  `virtual_stages` runs S stages inside one process (one GPU)
+with the same compress/decompress at every boundary; it is used for the loss
+parity test against the CPU oracle codec and as the N=1 point.
+"""
+from __future__ import annotations
+
+import math
+import os
+import time
+from dataclasses import dataclass, field
+from typing import Optional
+
+import torch
+import torch.distributed as dist
+import torch.nn as nn
+import torch.nn.functional as F
+
+from .compressor import CompressionPlan, adatopk_plan, select_k, uniform_plan
+from .transport import FrameCodec, frame_bytes
+
+_P2P_BATCHED = os.environ.get("GP_P2P_BATCHED", "1") == "1"  # batched single-op P2P (0: plain isend/irecv)
+
+
+@dataclass(frozen=True)
+class GPT2Config:
+    n_layer: int
+    n_embd: int
+    n_head: int
+    vocab: int = 50257
+    n_ctx: int = 1024
+
+
+GPT2_SMALL = GPT2Config(12, 768, 12)
+GPT2_MEDIUM = GPT2Config(24, 1024, 16)
+GPT2_XL = GPT2Config(48, 1600, 25)
+GPT2_TINY = GPT2Config(4, 128, 4, vocab=512, n_ctx=64)  # tests
+
+
+class Block(nn.Module):
+    def __init__(self, cfg: GPT2Config, sdpa: bool = True):
+        super().__init__()
+        h = cfg.n_embd
+        self.n_head = cfg.n_head
+        self.sdpa = sdpa
+        self.ln1 = nn.LayerNorm(h)
+        self.qkv = nn.Linear(h, 3 * h)
+        self.proj = nn.Linear(h, h)
+        self.ln2 = nn.LayerNorm(h)
+        self.fc = nn.Linear(h, 4 * h)
+        self.out = nn.Linear(4 * h, h)
+
+    def forward(self, x):
+        b, t, h = x.shape
+        q, k, v = self.qkv(self.ln1(x)).split(h, dim=2)
+        q, k, v = (z.view(b, t, self.n_head, h // self.n_head).transpose(1, 2) for z in (q, k, v))
+        if self.sdpa:
+            y = F.scaled_dot_product_attention(q, k, v, is_causal=True)
+        else:  # deterministic path for parity tests
+            att = (q @ k.transpose(-2, -1)) / math.sqrt(h // self.n_head)
+            att = att.masked_fill(torch.ones(t, t, dtype=torch.bool, device=x.device).triu(1), float("-inf"))
+            y = att.softmax(-1) @ v
+        x = x + self.proj(y.transpose(1, 2).reshape(b, t, h))
+        return x + self.out(F.gelu(self.fc(self.ln2(x)), approximate="tanh"))
+
+
+class Stage(nn.Module):
+    """Layers [a, b) of GPT-2, plus the embeddings (first) / final LN + head (last).
+
+    Every module is initialised from a seed keyed by its layer, so the weights
+    do not depend on the partition (as executor.py:161-178 keys parameters by
+    op name, not placement).
+    """
+
+    def __init__(self, cfg: GPT2Config, a: int, b: int, first: bool, last: bool, sdpa: bool = True, seed: int = 0):
+        super().__init__()
+        self.first, self.last = first, last
+        if first:
+            torch.manual_seed(seed * 7919 + 1)
+            self.wte = nn.Embedding(cfg.vocab, cfg.n_embd)
+            self.wpe = nn.Embedding(cfg.n_ctx, cfg.n_embd)
+        blocks = []
+        for i in range(a, b):
+            torch.manual_seed(seed * 7919 + 100 + i)
+            blocks.append(Block(cfg, sdpa))
+        self.blocks = nn.ModuleList(blocks)
+        if last:
+            torch.manual_seed(seed * 7919 + 2)
+            self.ln_f = nn.LayerNorm(cfg.n_embd)
+            self.head = nn.Linear(cfg.n_embd, cfg.vocab, bias=False)
+
+    def forward(self, x, targets=None):
+        if self.first:
+            pos = torch.arange(x.shape[1], device=x.device)
+            x = self.wte(x) + self.wpe(pos)
+        for blk in self.blocks:
+            x = blk(x)
+        if self.last:
+            logits = self.head(self.ln_f(x)).float()
+            return F.cross_entropy(logits.view(-1, logits.shape[-1]), targets.view(-1))
+        return x
+
+
+def partition(n_layer: int, n_stages: int):
+    """Contiguous, equal split of the layer chain (OP-Fence on a homogeneous chain)."""
+    bounds = [round(i * n_layer / n_stages) for i in range(n_stages + 1)]
+    return [(bounds[i], bounds[i + 1]) for i in range(n_stages)]
+
+
+def make_stage(cfg: GPT2Config, s: int, n_stages: int, device, seed: int = 0, sdpa: bool = True) -> Stage:
+    a, b = partition(cfg.n_layer, n_stages)[s]
+    return Stage(cfg, a, b, s == 0, s == n_stages - 1, sdpa, seed).to(device)
+
+
+def link_plan(n_stages: int, mode: str, ratio: float, link_times: Optional[list] = None) -> CompressionPlan:
+    """Per-link ratios for the chain 0-1-...-(S-1), both directions.
+
+    `mode` "adatopk": Eq. 6 over link communication times R (seconds), each FP
+    link's R mirrored onto its BP link (the reference's CLI keys FP links only,
+    SURVEY.md §7.10); "uniform": every link at `ratio`; "none": no plan.
+    """
+    if mode == "none" or n_stages < 2:
+        return None
+    links = [(s, s + 1) for s in range(n_stages - 1)] + [(s + 1, s) for s in range(n_stages - 1)]
+    if mode == "uniform":
+        return uniform_plan(links, ratio)
+    R = {}
+    for s in range(n_stages - 1):
+        t = link_times[s] if link_times is not None else 1.0
+        R[(s, s + 1)] = t
+        R[(s + 1, s)] = t
+    return adatopk_plan(None, R, ratio)
+
+
+def two_cluster_link_times(n_stages: int, boundary_bytes: int, fast=(1e-5, 1 / 100e9), slow=(5e-3, 1 / 1.25e9)):
+    """Simulated heterogeneous links (alpha + beta*M): two clusters of S/2
+    stages, fast links inside, one slow link between them (the style of the
+    reference's scenarios/fig7_clusters.json)."""
+    mid = n_stages // 2 - 1
+    return [(slow if s == mid else fast)[0] + (slow if s == mid else fast)[1] * boundary_bytes
+            for s in range(n_stages - 1)]
+
+
+@dataclass
+class PipelineStats:
+    step_ms: float = 0.0
+    loss: float = float("nan")
+    compress_calls: int = 0
+    wire_bytes: int = 0
+    dense_bytes: int = 0
+
+
+class VirtualPipeline:
+    """All S stages in one process/GPU, compressing at every boundary (fill-drain)."""
+
+    def __init__(self, cfg: GPT2Config, n_stages: int, plan: Optional[CompressionPlan], device, codec=None,
+                 lr: float = 1e-4, seed: int = 0, sdpa: bool = True):
+        self.cfg, self.S, self.plan, self.device = cfg, n_stages, plan, device
+        self.codec = codec if codec is not None else FrameCodec(device)
+        self.stages = [make_stage(cfg, s, n_stages, device, seed, sdpa) for s in range(n_stages)]
+        self.opts = [torch.optim.AdamW(st.parameters(), lr=lr) for st in self.stages]
+        self.stats = PipelineStats()
+
+    def _link(self, x: torch.Tensor, src: int, dst: int) -> torch.Tensor:
+        r = self.plan.ratio_for(src, dst) if self.plan is not None else 1.0
+        self.stats.dense_bytes += x.numel() * x.element_size()
+        if r <= 1.0:
+            self.stats.wire_bytes += x.numel() * x.element_size()
+            return x.detach().clone()
+        frame = self.codec.compress(x.detach().contiguous(), r)
+        self.stats.compress_calls += 1
+        self.stats.wire_bytes += frame.numel() - 16
+        out = torch.empty_like(x)
+        self.codec.decompress(frame, out, r)
+        return out
+
+    def step(self, tokens: torch.Tensor, targets: torch.Tensor, n_micro: int) -> float:
+        S = self.S
+        mbs = tokens.chunk(n_micro)
+        tgs = targets.chunk(n_micro)
+        acts = [[None] * S for _ in range(n_micro)]  # (input leaf, output) per stage
+        losses = []
+        for m in range(n_micro):  # fill: every micro-batch forward
+            x = mbs[m]
+            for s in range(S):
+                inp = x if s == 0 else x.requires_grad_(True)
+                with torch.autocast("cuda", dtype=torch.bfloat16):
+                    y = self.stages[s](inp, tgs[m] if s == S - 1 else None)
+                acts[m][s] = (inp, y)
+                if s < S - 1:
+                    x = self._link(y, s, s + 1)
+            losses.append(y)
+        for m in range(n_micro):  # drain: every micro-batch backward
+            grad = None
+            for s in range(S - 1, -1, -1):
+                inp, y = acts[m][s]
+                if s == S - 1:
+                    (y / n_micro).backward()
+                else:
+                    y.backward(grad)
+                if s > 0:
+                    grad = self._link(inp.grad, s, s - 1)
+        for o in self.opts:
+            o.step()
+            o.zero_grad(set_to_none=True)
+        loss = float(torch.stack([l.detach() for l in losses]).mean())
+        self.stats.loss = loss
+        return loss
+
+
+class DistPipeline:
+    """One stage per rank (torch.distributed, NCCL); fill-drain with compressed P2P."""
+
+    def __init__(self, cfg: GPT2Config, plan: Optional[CompressionPlan], micro_batch: int, seq_len: int,
+                 lr: float = 1e-4, seed: int = 0):
+        self.rank, self.S = dist.get_rank(), dist.get_world_size()
+        self.device = torch.device("cuda", torch.cuda.current_device())
+        self.cfg, self.plan, self.mb, self.T = cfg, plan, micro_batch, seq_len
+        self.stage = make_stage(cfg, self.rank, self.S, self.device, seed)
+        self.opt = torch.optim.AdamW(self.stage.parameters(), lr=lr)
+        self.codec = FrameCodec(self.device)
+        self.shape = (micro_batch, seq_len, cfg.n_embd)
+
+    def _ratio(self, src, dst):
+        return self.plan.ratio_for(src, dst) if self.plan is not None else 1.0
+
+    def _send(self, x: torch.Tensor, dst: int):
+        r = self._ratio(self.rank, dst)
+        buf = x.detach().contiguous() if r <= 1.0 else self.codec.compress(x.detach().contiguous(), r)
+        if _P2P_BATCHED:
+            return dist.batch_isend_irecv([dist.P2POp(dist.isend, buf, dst)])[0], buf
+        return dist.isend(buf, dst), buf
+
+    def _recv(self, src: int) -> torch.Tensor:
+        r = self._ratio(src, self.rank)
+        out = torch.empty(self.shape, device=self.device)
+        buf = out if r <= 1.0 else torch.empty(frame_bytes(out.numel(), r), dtype=torch.uint8, device=self.device)
+        if _P2P_BATCHED:
+            dist.batch_isend_irecv([dist.P2POp(dist.irecv, buf, src)])[0].wait()
+        else:
+            dist.irecv(buf, src).wait()
+        return out if r <= 1.0 else self.codec.decompress(buf, out, r)
+
+    def step(self, tokens: torch.Tensor, targets: torch.Tensor, n_micro: int):
+        s, S = self.rank, self.S
+        mbs, tgs = tokens.chunk(n_micro), targets.chunk(n_micro)
+        pending, saved, losses = [], [], []
+        for m in range(n_micro):  # fill
+            inp = mbs[m] if s == 0 else self._recv(s - 1).requires_grad_(True)
+            with torch.autocast("cuda", dtype=torch.bfloat16):
+                y = self.stage(inp, tgs[m] if s == S - 1 else None)
+            saved.append((inp, y))
+            if s < S - 1:
+                pending.append(self._send(y, s + 1))
+            else:
+                losses.append(y.detach())
+        for m in range(n_micro):  # drain
+            inp, y = saved[m]
+            if s == S - 1:
+                (y / n_micro).backward()
+            else:
+                y.backward(self._recv(s + 1))
+            if s > 0:
+                pending.append(self._send(inp.grad, s - 1))
+        for w, _buf in pending:
+            w.wait()
+        self.opt.step()
+        self.opt.zero_grad(set_to_none=True)
+        loss = torch.stack(losses).mean() if losses else torch.zeros((), device=self.device)
+        dist.broadcast(loss, S - 1)
+        return float(loss)
+
+
+MODELS = {"small": GPT2_SMALL, "medium": GPT2_MEDIUM, "xl": GPT2_XL}
+
+
+def run_pipeline(model: str = "medium", plan_mode: str = "uniform", ratio: float = 100.0, micro_batch: int = None,
+                 n_micro: int = None, seq_len: int = 1024, steps: int = 3, warmup: int = 1) -> dict:
+    """Time GPipe steps of GPT-2 with one stage per rank (or one stage on one GPU).
+
+    Returns samples/s = global batch / step time (CUDA events, max over ranks).
+    Call after torch.distributed is initialised when WORLD_SIZE > 1.
+    """
+    cfg = MODELS[model]
+    mb = micro_batch or (8 if model != "xl" else 4)
+    world = dist.get_world_size() if dist.is_initialized() else 1
+    n_micro = n_micro or max(4, 2 * world)
+    dev = torch.device("cuda", torch.cuda.current_device())
+    boundary = mb * seq_len * cfg.n_embd
+    lt = two_cluster_link_times(world, boundary * 4) if plan_mode == "adatopk" else None
+    plan = link_plan(world, plan_mode, ratio, lt)
+    pipe = DistPipeline(cfg, plan, mb, seq_len) if world > 1 else VirtualPipeline(cfg, 1, None, dev)
+    gb = mb * n_micro
+    times, loss = [], float("nan")
+    for i in range(warmup + steps):
+        tok, tgt = synthetic_batch(cfg, gb, seq_len, dev, seed=i)
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        loss = pipe.step(tok, tgt, n_micro)
+        b.record()
+        torch.cuda.synchronize()
+        if i >= warmup:
+            times.append(a.elapsed_time(b))
+    t = sum(times) / len(times)
+    if world > 1:
+        tt = torch.tensor([t], device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        t = float(tt.item())
+    links = {}
+    if plan is not None:
+        for (s, d), r in sorted(plan.per_link.items()):
+            links[f"{s}->{d}"] = {"ratio": round(r, 3), "k": select_k(boundary, r),
+                                  "wire_bytes": 16 + 12 * select_k(boundary, r)}
+    del pipe
+    torch.cuda.empty_cache()
+    return {"metric": "GPT-2 compressed-pipeline samples/s", "value": round(gb / (t * 1e-3), 3), "unit": "samples/s",
+            "n_gpus": world, "model": model, "layers": cfg.n_layer, "hidden": cfg.n_embd, "micro_batch": mb,
+            "n_micro": n_micro, "global_batch": gb, "seq_len": seq_len, "ms_per_step": round(t, 2),
+            "loss": round(loss, 4), "plan": plan_mode if world > 1 else "none (1 stage, no boundary)",
+            "base_ratio": ratio, "boundary_elems": boundary, "dense_boundary_bytes": boundary * 4, "links": links,
+            "schedule": "GPipe fill-drain (executor.py:389-404), bf16 autocast, fp32 boundaries",
+            "partition": "contiguous equal layers (OP-Fence split of a homogeneous chain)",
+            "data": "synthetic tokens, random init"}
+
+
+def synthetic_batch(cfg: GPT2Config, batch: int, seq_len: int, device, seed: int = 0):
+    g = torch.Generator(device=device).manual_seed(seed)
+    tok = torch.randint(0, cfg.vocab, (batch, seq_len + 1), device=device, generator=g)
+    return tok[:, :-1].contiguous(), tok[:, 1:].contiguous()
+
+
+__all__ = ["GPT2Config", "GPT2_SMALL", "GPT2_MEDIUM", "GPT2_XL", "GPT2_TINY", "partition", "make_stage",
+           "link_plan", "two_cluster_link_times", "VirtualPipeline", "DistPipeline", "synthetic_batch", "run_pipeline",
+           ]
