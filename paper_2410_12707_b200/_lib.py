@@ -6,10 +6,11 @@ entry point fails loudly.
 from __future__ import annotations
 
 import ctypes
+import os
 from ctypes import c_double, c_int, c_int32, c_int64, c_size_t, c_void_p, POINTER
 from pathlib import Path
 
-LIB_PATH = Path(__file__).resolve().parent / "_lib" / "libadatopk.so"
+LIB_PATH = Path(os.environ.get("GP_LIB") or Path(__file__).resolve().parent / "_lib" / "libadatopk.so")
 
 DTYPE_F32 = 0
 DTYPE_BF16 = 1

@@ -42,33 +42,35 @@ def _stale(target: Path, deps: list[Path]) -> bool:
     return any(p.stat().st_mtime > t for p in deps)
 
 
-def build(force: bool = False, verbose: bool = False) -> Path:
-    OUT_DIR.mkdir(exist_ok=True)
+def build(force: bool = False, verbose: bool = False, out_dir: Path = OUT_DIR, defines=()) -> Path:
+    """Compile the library; `out_dir`/`defines` build development variants (see scripts/build_variant.py)."""
+    out_dir.mkdir(parents=True, exist_ok=True)
+    lib_path = out_dir / LIB.name
     headers = sorted(CSRC.glob("*.cuh")) + [ROOT / "include" / "adatopk.h"]
     objs = []
     log = []
     for src in SOURCES:
         s = CSRC / src
-        o = OUT_DIR / (s.stem + ".o")
+        o = out_dir / (s.stem + ".o")
         objs.append(o)
         if force or _stale(o, [s, *headers]):
-            cmd = [nvcc(), *ARCH, *COMMON, *PER_FILE.get(src, []), "-Xptxas", "-v", "-c", str(s), "-o", str(o)]
+            cmd = [nvcc(), *ARCH, *COMMON, *defines, *PER_FILE.get(src, []), "-Xptxas", "-v", "-c", str(s), "-o", str(o)]
             r = subprocess.run(cmd, capture_output=True, text=True)
             log.append(r.stdout + r.stderr)
             if r.returncode != 0:
                 sys.stderr.write(r.stdout + r.stderr)
                 raise RuntimeError(f"nvcc failed on {src}")
-    if force or _stale(LIB, objs):
-        cmd = [nvcc(), *ARCH, "-shared", "-o", str(LIB), *map(str, objs), "-lcudart"]
+    if force or _stale(lib_path, objs):
+        cmd = [nvcc(), *ARCH, "-shared", "-o", str(lib_path), *map(str, objs), "-lcudart"]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             sys.stderr.write(r.stdout + r.stderr)
             raise RuntimeError("nvcc link failed")
     if log:
-        (OUT_DIR / "ptxas.log").write_text("\n".join(log))
+        (out_dir / "ptxas.log").write_text("\n".join(log))
     if verbose and log:
         print("\n".join(log))
-    return LIB
+    return lib_path
 
 
 if __name__ == "__main__":

@@ -45,11 +45,14 @@
 
 #include "gp_kernels.cuh"
 
+#ifndef GP_LIST_KB
+#define GP_LIST_KB 40
+#endif
+
 namespace gp {
 
-constexpr int kListBytes = 40 * 1024;  // per-CTA shared-memory candidate lists
 constexpr int kMaxGridSpec = 160;      // largest grid: the one-round-trip FC gather stages G*32 keys in smem
-constexpr int kRowsPerBuf = 2;         // rows per pipeline buffer (x2 buffers in flight)
+constexpr uint32_t kRing = 4;          // 1 KiB rows in flight per warp (bulk copies into smem)
 
 // ---------------------------------------------------------------------------
 // list entries: (global index, raw bits) — 8 B for 16/32-bit, 16 B for 64-bit
@@ -57,6 +60,9 @@ constexpr int kRowsPerBuf = 2;         // rows per pipeline buffer (x2 buffers i
 template <class Tr>
 struct Entry {
   static constexpr uint32_t kBytes = sizeof(typename Tr::Bits) == 4 ? 8 : 16;
+  // per-CTA shared-memory candidate lists (a larger list starves L1, where
+  // the few register spills of the stream loop live)
+  static constexpr uint32_t kListBytes = GP_LIST_KB * 1024;
   static constexpr uint32_t kSmemCap = kListBytes / (32 * kBytes);  // entries per warp in smem
 
   __device__ __forceinline__ static void put(unsigned char* base, uint32_t pos, uint32_t idx, typename Tr::Bits b) {
@@ -97,44 +103,55 @@ struct WarpList {
   }
 };
 
+// Visit entries [j0, L) of a warp's list in index order, 32 per step, with
+// the loads of kScanDepth steps in flight (spilled entries live in L2/HBM: one
+// round trip per step would serialise the pass).  body(valid, idx, bits) runs
+// warp-wide.
+#ifndef GP_SCAN_DEPTH
+#define GP_SCAN_DEPTH 4
+#endif
+constexpr int kScanDepth = GP_SCAN_DEPTH;
+template <class Tr, class F>
+__device__ __forceinline__ void list_scan(const WarpList<Tr>& list, uint32_t L, F&& body, uint32_t j0 = 0) {
+  const uint32_t lane = threadIdx.x & 31;
+  for (uint32_t base = j0; base < L; base += kScanDepth * 32u) {
+    uint32_t idx[kScanDepth];
+    typename Tr::Bits b[kScanDepth];
+#pragma unroll
+    for (int q = 0; q < kScanDepth; ++q) {
+      const uint32_t j = base + q * 32u + lane;
+      idx[q] = 0;
+      b[q] = 0;
+      if (j < L) list.get(j, idx[q], b[q]);
+    }
+#pragma unroll
+    for (int q = 0; q < kScanDepth; ++q)
+      if (base + q * 32u < L) body(base + q * 32u + lane < L, idx[q], b[q]);
+  }
+}
+
 template <class Tr>
 __device__ __forceinline__ typename Tr::Bits load_bits(const void* x, uint32_t i) {
   return (typename Tr::Bits)__ldg(reinterpret_cast<const typename Tr::Elem*>(x) + i);
 }
 
 // ---------------------------------------------------------------------------
-// 32-byte lane chunks
+// one element's raw bits from shared memory
 
-__device__ __forceinline__ void ld_chunk(const uint32_t* p, uint32_t (&v)[8]) {
-  asm volatile("ld.global.nc.L1::no_allocate.v8.u32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
-               : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7])
-               : "l"(p));
-}
-
-// element e of a chunk; e may be a runtime value (select chain, no local memory)
 template <class Tr>
-__device__ __forceinline__ typename Tr::Bits chunk_elem(const uint32_t (&v)[8], uint32_t e) {
+__device__ __forceinline__ typename Tr::Bits ld_shared_elem(uint32_t addr) {
   if constexpr (sizeof(typename Tr::Elem) == 4) {
-    uint32_t r = v[0];
-#pragma unroll
-    for (int i = 1; i < 8; ++i)
-      if (e == (uint32_t)i) r = v[i];
-    return r;
+    uint32_t v;
+    asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(addr));
+    return v;
   } else if constexpr (sizeof(typename Tr::Elem) == 2) {
-    uint32_t r = v[0];
-#pragma unroll
-    for (int i = 1; i < 8; ++i)
-      if ((e >> 1) == (uint32_t)i) r = v[i];
-    return (e & 1) ? (r >> 16) : (r & 0xFFFFu);
+    uint16_t v;
+    asm volatile("ld.shared.u16 %0, [%1];" : "=h"(v) : "r"(addr));
+    return (typename Tr::Bits)v;
   } else {
-    uint32_t lo = v[0], hi = v[1];
-#pragma unroll
-    for (int i = 1; i < 4; ++i)
-      if (e == (uint32_t)i) {
-        lo = v[2 * i];
-        hi = v[2 * i + 1];
-      }
-    return (typename Tr::Bits)(((uint64_t)hi << 32) | lo);
+    uint64_t v;
+    asm volatile("ld.shared.u64 %0, [%1];" : "=l"(v) : "r"(addr));
+    return v;
   }
 }
 
@@ -199,6 +216,9 @@ __device__ __forceinline__ bool warp_cross_desc(const uint32_t* hist, int top, u
 template <class Tr>
 __device__ __forceinline__ void write_out(const CompressArgs& a, uint32_t pos, uint32_t idx, typename Tr::Bits b) {
   using Elem = typename Tr::Elem;
+#ifdef GP_EXP_NOWRITE
+  if (idx != 0xFFFFFFFFu) return;
+#endif
   if (a.idx64) reinterpret_cast<int64_t*>(a.idx_out)[pos] = (int64_t)idx;
   else reinterpret_cast<int32_t*>(a.idx_out)[pos] = (int32_t)idx;
   if (a.val_f32) reinterpret_cast<float*>(a.val_out)[pos] = Tr::to_f32(b);
@@ -235,10 +255,15 @@ struct Smem {
   static constexpr size_t res = s32 + 64 * 4;                           // 32 u32
   static constexpr size_t warp = res + 32 * 4;                          // 4 x 32 u32
   static constexpr size_t fcoff = warp + 4 * 32 * 4;                    // kMaxGrid+4 u32
-  static constexpr size_t fcpre = fcoff + (kMaxGrid + 4) * 4;           // kFcCap+4 u32
+  static constexpr size_t mbar = (fcoff + (kMaxGrid + 4) * 4 + 7) & ~size_t(7);  // 32 x kRing mbarriers
+  static constexpr size_t ring = (mbar + 32 * kRing * 8 + 127) & ~size_t(127);   // 32 x kRing x 1 KiB rows
+  // the final-candidate arrays are used only after the stream: they alias the ring
+  static constexpr size_t fcpre = ring;                                           // kFcCap+4 u32
   static constexpr size_t fckey = (fcpre + (kFcCap + 4) * 4 + 15) & ~size_t(15);  // kFcCap keys
-  static constexpr size_t list = fckey + kFcCap * sizeof(typename Tr::Key);       // kListBytes
-  static constexpr size_t total = list + kListBytes;
+  static_assert(fckey + kFcCap * sizeof(typename Tr::Key) <= ring + 32 * kRing * 1024, "FC arrays fit the ring");
+  static constexpr size_t list = ring + 32 * kRing * 1024;                        // Entry::kListBytes
+  static constexpr size_t total = list + Entry<Tr>::kListBytes;
+  static_assert(total <= 227 * 1024, "shared memory");
 };
 
 // ---------------------------------------------------------------------------
@@ -252,7 +277,7 @@ __global__ void __launch_bounds__(kCompressThreads, 1) compress_kernel(const Com
   using SL = Smem<Tr>;
   constexpr int CS = Tr::kKeyBits - 12;        // coarse bin = key >> CS (12 bits)
   constexpr int EPL = 32 / (int)sizeof(Elem);  // elements per lane chunk (8 f32, 16 bf16, 4 f64)
-  constexpr int RB = kRowsPerBuf;
+  constexpr int EPS = 16 / (int)sizeof(Elem);  // elements per 16-byte piece
   constexpr uint32_t kEntryBytes = Entry<Tr>::kBytes;
   const int FB = a.fb;                         // fine-histogram bits
   const int FS = Tr::kKeyBits - FB;            // fine bin = key >> FS
@@ -294,25 +319,27 @@ __global__ void __launch_bounds__(kCompressThreads, 1) compress_kernel(const Com
     a.header[1] = (unsigned long long)k;
   }
 
-  // ---- the unit's first two buffers (4 rows) are requested before anything else
+  // ---- the unit's rows (1 KiB each) stream through a per-warp ring of
+  // kRing shared-memory slots, filled by bulk (TMA) copies on one mbarrier per
+  // slot; the first kRing rows are requested before anything else
   const uint32_t nch = a.aligned ? n / EPL : 0u;  // full 32-byte chunks in the unit
   const uint32_t nrow = (nch + 31) / 32;
   const uint32_t* xw = reinterpret_cast<const uint32_t*>(x + u0);
-  uint32_t cur[RB][8], nxt[RB][8];
-  auto load_rows = [&](uint32_t(&buf)[RB][8], uint32_t r0) {
-#pragma unroll
-    for (int rr = 0; rr < RB; ++rr) {
-      const uint32_t ch = (r0 + rr) * 32u + lane;
-      if (ch < nch) {
-        ld_chunk(xw + (size_t)ch * 8, buf[rr]);
-      } else {
-#pragma unroll
-        for (int i = 0; i < 8; ++i) buf[rr][i] = 0u;
-      }
-    }
+  const uint32_t ring = smem_addr(smem + SL::ring) + w * (kRing * 1024u);
+  const uint32_t mbar = smem_addr(smem + SL::mbar) + w * (kRing * 8u);
+  const uint64_t policy = l2_evict_first_policy();  // x is read once: keep L2 for the lists
+  uint32_t seq = 0;                                 // rows this warp has issued into the ring
+  auto issue = [&](uint32_t r, uint32_t q) {        // lane 0: row r as ring sequence number q
+    const uint32_t slot = q % kRing;
+    bulk_load_async(ring + slot * 1024u, xw + (size_t)r * 256u, min(32u, nch - r * 32u) * 32u, mbar + slot * 8u,
+                    policy);
   };
-  if (nrow > 0) load_rows(cur, 0);
-  if (nrow > RB) load_rows(nxt, RB);
+  if (lane == 0) {
+    for (uint32_t s = 0; s < kRing; ++s) mbar_init(mbar + s * 8u, 1u);
+    fence_mbar_init();
+    for (uint32_t r = 0; r < min(nrow, kRing); ++r) issue(r, r);
+  }
+  __syncwarp();
 
   // ---- stage 0: low watermark from this CTA's own first rows (no extra traffic)
   for (uint32_t i = tid; i < kCoarseBins; i += kCompressThreads) sh_coarse[i] = 0u;
@@ -320,12 +347,16 @@ __global__ void __launch_bounds__(kCompressThreads, 1) compress_kernel(const Com
   __syncthreads();
   {
     uint32_t ns = 0;
+    for (uint32_t r = 0; r < min(nrow, 2u); ++r) {
+      mbar_wait(mbar + r * 8u, 0u);
 #pragma unroll
-    for (int rr = 0; rr < RB; ++rr) {
-      if ((uint32_t)rr * 32u + lane < nch) {
-        atomicAdd(&sh_coarse[(uint32_t)(Tr::key(chunk_elem<Tr>(cur[rr], 0)) >> CS)], 1u);
-        atomicAdd(&sh_coarse[(uint32_t)(Tr::key(chunk_elem<Tr>(cur[rr], EPL / 2)) >> CS)], 1u);
-        ns += 2;
+      for (int h = 0; h < 2; ++h) {
+        const uint32_t piece = h * 32u + lane;  // 16-byte piece of the row
+        if (piece < 2u * (nch - r * 32u)) {
+          const uint4 v = ld_shared_v4(ring + r * 1024u + piece * 16u);
+          atomicAdd(&sh_coarse[(uint32_t)(Tr::key(Tr::lane(v, 0)) >> CS)], 1u);
+          ++ns;
+        }
       }
     }
     ns = warp_sum(ns);
@@ -404,59 +435,75 @@ __global__ void __launch_bounds__(kCompressThreads, 1) compress_kernel(const Com
     const typename Tr::Cand test = Tr::make_cand(lo_m1);
     const bool all = lo == 0;  // every element is a candidate, NaN included
     // the warp histograms the entries it just appended, one per lane
+    // Entries that spilled to global memory are histogrammed after the loop
+    // (reading them back here would put an L2 round trip on every row pair).
+    constexpr uint32_t kCap = Entry<Tr>::kSmemCap;
     auto count_new = [&](uint32_t from) {
       __syncwarp();
-      for (uint32_t j = from + lane; j < L; j += 32u) {
+      const uint32_t end = min(L, kCap);
+      for (uint32_t j = from + lane; j < end; j += 32u) {
         uint32_t idx;
         Bits b;
         list.get(j, idx, b);
         count(b);
       }
     };
-    auto process = [&](const uint32_t(&buf)[RB][8], uint32_t r0) {
-      uint32_t m[RB];
+    // one 1 KiB row from ring slot `so`: lane holds 16-byte pieces h*32+lane
+    // (h = 0, 1), i.e. elements [h*32*EPS + lane*EPS, +EPS) of the row
+    auto process = [&](uint32_t r, uint32_t so) {
+      const uint32_t npieces = 2u * min(32u, nch - r * 32u);
+      uint32_t m[2];
 #pragma unroll
-      for (int rr = 0; rr < RB; ++rr) {
+      for (int h = 0; h < 2; ++h) {
+        const uint32_t piece = h * 32u + lane;
         uint32_t mm = 0;
+        if (piece < npieces) {
+          const uint4 v = ld_shared_v4(so + piece * 16u);
 #pragma unroll
-        for (int e = 0; e < EPL; ++e)
-          if (all || test(chunk_elem<Tr>(buf[rr], e))) mm |= 1u << e;
-        m[rr] = ((r0 + rr) * 32u + lane < nch) ? mm : 0u;
+          for (int e = 0; e < EPS; ++e)
+            if (all || test(Tr::lane(v, e))) mm |= 1u << e;
+        }
+        m[h] = mm;
       }
-      static_assert(RB == 2, "packed two-row scan");
       const uint32_t packed = __popc(m[0]) | (__popc(m[1]) << 16);
       if (__any_sync(kFull, packed)) {
         const uint32_t incl = warp_incl_scan(packed);
         const uint32_t excl = incl - packed, tot = __shfl_sync(kFull, incl, 31);
-        uint32_t pos[RB] = {L + (excl & 0xFFFFu), L + (tot & 0xFFFFu) + (excl >> 16)};
         const uint32_t from = L;
+        uint32_t pos[2] = {L + (excl & 0xFFFFu), L + (tot & 0xFFFFu) + (excl >> 16)};
         L += (tot & 0xFFFFu) + (tot >> 16);
+        // append (divergent): each candidate is one LDS from the ring slot
 #pragma unroll
-        for (int rr = 0; rr < RB; ++rr) {  // divergent part: append only
-          uint32_t mm = m[rr];
-          const uint32_t base = u0 + ((r0 + rr) * 32u + lane) * EPL;
+        for (int h = 0; h < 2; ++h) {
+          uint32_t mm = m[h];
+          const uint32_t piece = h * 32u + lane;
+          const uint32_t base = u0 + r * (32u * EPL) + piece * EPS;
+          const uint32_t src = so + piece * 16u;
           while (mm) {
             const uint32_t e = __ffs(mm) - 1;
             mm &= mm - 1;
-            list.put(pos[rr]++, base + e, chunk_elem<Tr>(buf[rr], e));
+            list.put(pos[h]++, base + e, ld_shared_elem<Tr>(src + e * (uint32_t)sizeof(Elem)));
           }
         }
         count_new(from);
       }
     };
-    if (!preloaded) {
-      if (nrow > 0) load_rows(cur, 0);
-      if (nrow > RB) load_rows(nxt, RB);
+    const uint32_t q0 = seq;
+    if (!preloaded && lane == 0) {
+      fence_proxy_async_smem();
+      for (uint32_t r = 0; r < min(nrow, kRing); ++r) issue(r, q0 + r);
     }
-    // two buffers in flight: while one is being filtered the other is loading
-    for (uint32_t r0 = 0; r0 < nrow; r0 += 2 * RB) {
-      process(cur, r0);
-      if (r0 + 2 * RB < nrow) load_rows(cur, r0 + 2 * RB);
-      if (r0 + RB < nrow) {
-        process(nxt, r0 + RB);
-        if (r0 + 3 * RB < nrow) load_rows(nxt, r0 + 3 * RB);
+    for (uint32_t r = 0; r < nrow; ++r) {
+      const uint32_t q = q0 + r, slot = q % kRing;
+      mbar_wait(mbar + slot * 8u, (q / kRing) & 1u);
+      process(r, ring + slot * 1024u);
+      __syncwarp();
+      if (lane == 0 && r + kRing < nrow) {  // refill the slot just consumed
+        fence_proxy_async_smem();
+        issue(r + kRing, q + kRing);
       }
     }
+    seq = q0 + nrow;
     const Key span = lo ? Tr::kInfAbs - lo_m1 : ~(Key)0;
     for (uint32_t i0 = nch * EPL; i0 < n; i0 += 32u) {  // scalar tail / unaligned input
       const uint32_t i = i0 + lane;
@@ -472,6 +519,7 @@ __global__ void __launch_bounds__(kCompressThreads, 1) compress_kernel(const Com
       L += __popc(mk);
       count_new(from);
     }
+    list_scan<Tr>(list, L, [&](bool valid, uint32_t, Bits b) { if (valid) count(b); }, kCap);  // spilled tail
     mymax = __reduce_max_sync(kFull, mymax);
     if (lane == 0) {
       if (mymax) atomicMax(&sh_res[18], mymax);
@@ -559,36 +607,6 @@ __global__ void __launch_bounds__(kCompressThreads, 1) compress_kernel(const Com
   }
   STAMP(4);
 
-  // per-warp split of my candidates: sure (fine bin > B1) / final candidates (== B1)
-  {
-    uint32_t ca = 0, cb = 0;
-    for (uint32_t j = lane; j < L; j += 32u) {
-      uint32_t idx;
-      Bits b;
-      list.get(j, idx, b);
-      const uint32_t fb = (uint32_t)(Tr::key(b) >> FS);
-      ca += fb > B1;
-      cb += fb == B1;
-    }
-    ca = warp_sum(ca);
-    cb = warp_sum(cb);
-    if (lane == 0) {
-      w_a[w] = ca;
-      w_b[w] = cb;
-    }
-  }
-  __syncthreads();
-  if (w == 0) {
-    const uint32_t va = w_a[lane], vb = w_b[lane];
-    const uint32_t ia = warp_incl_scan(va), ib = warp_incl_scan(vb);
-    w_aoff[lane] = ia - va;
-    w_boff[lane] = ib - vb;
-    if (lane == 31) {
-      sh_res[8] = ia;
-      sh_res[9] = ib;
-    }
-  }
-  __syncthreads();
   // bf16: the bits below the fine bin are constant, so B1 already is the key
   // (except bin 0, which holds both NaN, key 0, and +-0, key 1)
   const bool kDirectT = Tr::kDirectT && B1 != 0;
@@ -599,22 +617,63 @@ __global__ void __launch_bounds__(kCompressThreads, 1) compress_kernel(const Com
     // index order, so one coalesced read of 32 words per CTA after B2 returns
     // every count and (usually) every key.
     Key* fcreg = reinterpret_cast<Key*>(a.fcreg) + (size_t)c * kFcCap;
-    if (!kDirectT) {
-      uint32_t j0 = 2 + w_boff[w];
-      for (uint32_t base = 0; base < L; base += 32u) {
-        const uint32_t j = base + lane;
-        bool isfc = false;
-        Key kk = 0;
-        if (j < L) {
-          uint32_t idx;
-          Bits b;
-          list.get(j, idx, b);
-          kk = Tr::key(b);
-          isfc = (uint32_t)(kk >> FS) == B1;
+    // One pass over the list: per-warp sure / FC counts, with the FC keys
+    // staged in the (still unused) FC smem, kStageW per warp.
+    constexpr uint32_t kStageW = kFcCap / 32;
+    Key* stagew = sh_fckey + w * kStageW;
+    {
+      uint32_t ca = 0, cb = 0;
+      list_scan<Tr>(list, L, [&](bool valid, uint32_t, Bits b) {
+        const Key kk = Tr::key(b);
+        const uint32_t fb = (uint32_t)(kk >> FS);
+        const bool isfc = valid && fb == B1;
+        const uint32_t fm = __ballot_sync(kFull, isfc);
+        ca += __popc(__ballot_sync(kFull, valid && fb > B1));
+        if (!kDirectT && isfc) {
+          const uint32_t p = cb + __popc(fm & lanemask_lt());
+          if (p < kStageW) stagew[p] = kk;
         }
-        const uint32_t mk = __ballot_sync(kFull, isfc);
-        if (isfc) fcreg[j0 + __popc(mk & lanemask_lt())] = kk;
-        j0 += __popc(mk);
+        cb += __popc(fm);
+      });
+      if (lane == 0) {
+        w_a[w] = ca;
+        w_b[w] = cb;
+      }
+    }
+    __syncthreads();
+    if (w == 0) {
+      const uint32_t va = w_a[lane], vb = w_b[lane];
+      const uint32_t ia = warp_incl_scan(va), ib = warp_incl_scan(vb);
+      w_aoff[lane] = ia - va;
+      w_boff[lane] = ib - vb;
+      if (lane == 31) {
+        sh_res[8] = ia;
+        sh_res[9] = ib;
+      }
+    }
+    __syncthreads();
+    if (!kDirectT) {  // publish the staged keys at the warp's place in the CTA's index order
+      const uint32_t cb = w_b[w];
+      Key* dst = fcreg + 2 + w_boff[w];
+      for (uint32_t i = lane; i < min(cb, kStageW); i += 32u) dst[i] = stagew[i];
+      if (cb > kStageW) {  // rare: this warp alone holds more than its staging share
+        uint32_t r = 0;
+        for (uint32_t base = 0; base < L; base += 32u) {
+          const uint32_t j = base + lane;
+          bool isfc = false;
+          Key kk = 0;
+          if (j < L) {
+            uint32_t idx;
+            Bits b;
+            list.get(j, idx, b);
+            kk = Tr::key(b);
+            isfc = (uint32_t)(kk >> FS) == B1;
+          }
+          const uint32_t fm = __ballot_sync(kFull, isfc);
+          const uint32_t p = r + __popc(fm & lanemask_lt());
+          if (isfc && p >= kStageW) dst[p] = kk;
+          r += __popc(fm);
+        }
       }
     }
     if (tid == 0) {
@@ -675,16 +734,33 @@ __global__ void __launch_bounds__(kCompressThreads, 1) compress_kernel(const Com
     if (kDirectT) {
       T |= 1;  // every FC key equals T; the tie quota is the whole need
     } else {
-      // place the index-ordered FC list: staged keys first, then the rest of
-      // any CTA holding more than kSpec-2 (rare second round trip)
-      for (uint32_t s = tid; s < G * kSpec; s += kCompressThreads) {
-        const uint32_t c2 = s / kSpec, j = s % kSpec;
-        if (j >= 2 && j - 2 < (uint32_t)stage[c2 * kSpec + 1]) sh_fckey[sh_fcoff[c2] + j - 2] = stage[s];
-      }
-      for (uint32_t c2 = w; c2 < G; c2 += 32u) {
-        const uint32_t cnt = sh_fcoff[c2 + 1] - sh_fcoff[c2];
-        const Key* src = reinterpret_cast<const Key*>(a.fcreg) + (size_t)c2 * kFcCap + 2;
-        for (uint32_t j = kSpec - 2 + lane; j < cnt; j += 32u) sh_fckey[sh_fcoff[c2] + j] = src[j];
+      // place the index-ordered FC list: position p belongs to the last CTA
+      // whose offset is <= p; ranks beyond the staged kSpec-2 keys take one
+      // more (independent) load, so a big FC list costs one extra round trip
+      {
+        constexpr int PER = kFcCap / kCompressThreads;
+        const Key* fcall = reinterpret_cast<const Key*>(a.fcreg);
+        Key v[PER];
+#pragma unroll
+        for (int i = 0; i < PER; ++i) {
+          const uint32_t p = tid + i * kCompressThreads;
+          v[i] = 0;
+          if (p < Mt) {
+            uint32_t lo = 0, hi = G;  // sh_fcoff[lo] <= p < sh_fcoff[hi]
+            while (hi - lo > 1u) {
+              const uint32_t mid = (lo + hi) >> 1;
+              if (sh_fcoff[mid] <= p) lo = mid;
+              else hi = mid;
+            }
+            const uint32_t j = p - sh_fcoff[lo];
+            v[i] = j < kSpec - 2 ? stage[lo * kSpec + 2 + j] : fcall[(size_t)lo * kFcCap + 2 + j];
+          }
+        }
+#pragma unroll
+        for (int i = 0; i < PER; ++i) {
+          const uint32_t p = tid + i * kCompressThreads;
+          if (p < Mt) sh_fckey[p] = v[i];
+        }
       }
       __syncthreads();
       // in-smem radix select over the low FS bits of the final candidates
@@ -748,18 +824,9 @@ __global__ void __launch_bounds__(kCompressThreads, 1) compress_kernel(const Com
     const uint32_t fcw = fc_c + w_boff[w];
     uint32_t o = sure_off + fcsel(fc_c) + w_aoff[w] + (fcsel(fcw) - fcsel(fc_c));
     uint32_t jfc = fcw;
-    for (uint32_t base = 0; base < L; base += 32u) {
-      const uint32_t j = base + lane;
-      uint32_t idx = 0;
-      Bits b = 0;
-      Key kk = 0;
-      uint32_t fb = 0;
-      const bool valid = j < L;
-      if (valid) {
-        list.get(j, idx, b);
-        kk = Tr::key(b);
-        fb = (uint32_t)(kk >> FS);
-      }
+    list_scan<Tr>(list, L, [&](bool valid, uint32_t idx, Bits b) {
+      const Key kk = Tr::key(b);
+      const uint32_t fb = (uint32_t)(kk >> FS);
       const bool isfc = valid && fb == B1;
       const uint32_t fm = __ballot_sync(kFull, isfc);
       const uint32_t p = jfc + __popc(fm & lanemask_lt());
@@ -771,7 +838,7 @@ __global__ void __launch_bounds__(kCompressThreads, 1) compress_kernel(const Com
       if (sel) write_out<Tr>(a, o + __popc(sm & lanemask_lt()), idx, b);
       o += __popc(sm);
       jfc += __popc(fm);
-    }
+    });
   } else {
     // ================= slow path: many keys share the fine bin B1 =================
     uint32_t need = k - G1;
@@ -785,13 +852,10 @@ __global__ void __launch_bounds__(kCompressThreads, 1) compress_kernel(const Com
         const int lob = hib - nb;
         if (tid < 256) sh_lvl[tid] = 0u;
         __syncthreads();
-        for (uint32_t j = lane; j < L; j += 32u) {
-          uint32_t idx;
-          Bits b;
-          list.get(j, idx, b);
+        list_scan<Tr>(list, L, [&](bool valid, uint32_t, Bits b) {
           const Key kk = Tr::key(b);
-          if ((kk >> hib) == (T >> hib)) atomicAdd(&sh_lvl[(uint32_t)(kk >> lob) & ((1u << nb) - 1u)], 1u);
-        }
+          if (valid && (kk >> hib) == (T >> hib)) atomicAdd(&sh_lvl[(uint32_t)(kk >> lob) & ((1u << nb) - 1u)], 1u);
+        });
         __syncthreads();
         if (tid < 256 && sh_lvl[tid]) red_add_gpu(&a.hist_lvl[lvl * 256 + tid], sh_lvl[tid]);
         grid_barrier(bar, G);
@@ -814,14 +878,11 @@ __global__ void __launch_bounds__(kCompressThreads, 1) compress_kernel(const Com
     const uint32_t need_eq = need;
     {
       uint32_t gt = 0, eq = 0;
-      for (uint32_t j = lane; j < L; j += 32u) {
-        uint32_t idx;
-        Bits b;
-        list.get(j, idx, b);
+      list_scan<Tr>(list, L, [&](bool valid, uint32_t, Bits b) {
         const Key kk = Tr::key(b);
-        gt += kk > T;
-        eq += kk == T;
-      }
+        gt += valid && kk > T;
+        eq += valid && kk == T;
+      });
       gt = warp_sum(gt);
       eq = warp_sum(eq);
       if (lane == 0) {
@@ -857,16 +918,8 @@ __global__ void __launch_bounds__(kCompressThreads, 1) compress_kernel(const Com
     const uint32_t eqw = eq_c + w_boff[w];
     uint32_t o = gt_c + min(eq_c, need_eq) + w_aoff[w] + (min(eqw, need_eq) - min(eq_c, need_eq));
     uint32_t er = eqw;
-    for (uint32_t base = 0; base < L; base += 32u) {
-      const uint32_t j = base + lane;
-      uint32_t idx = 0;
-      Bits b = 0;
-      Key kk = 0;
-      const bool valid = j < L;
-      if (valid) {
-        list.get(j, idx, b);
-        kk = Tr::key(b);
-      }
+    list_scan<Tr>(list, L, [&](bool valid, uint32_t idx, Bits b) {
+      const Key kk = Tr::key(b);
       const bool iseq = valid && kk == T;
       const uint32_t em = __ballot_sync(kFull, iseq);
       const bool sel = valid && (kk > T || (iseq && er + __popc(em & lanemask_lt()) < need_eq));
@@ -874,7 +927,7 @@ __global__ void __launch_bounds__(kCompressThreads, 1) compress_kernel(const Com
       if (sel) write_out<Tr>(a, o + __popc(sm & lanemask_lt()), idx, b);
       o += __popc(sm);
       er += __popc(em);
-    }
+    });
     if (c == 0) {
       for (uint32_t i = tid; i < (uint32_t)(lvl * 256); i += kCompressThreads) a.hist_lvl[i] = 0u;
     }

@@ -5,6 +5,7 @@ between graphs with and without the op, so CPU launch latency is excluded and
 every op starts cold (a 512 MB read flushes L2 between iterations).
 """
 import ctypes
+import os
 import statistics
 import sys
 from pathlib import Path
@@ -59,6 +60,9 @@ def main():
               ("resnet 64x2048x7x7", (64, 2048, 7, 7), "f32"), ("resnet 64x512x28x28", (64, 512, 28, 28), "f32"),
               ("resnet 64x256x56x56", (64, 256, 56, 56), "f32"), ("C3 bf16 8x1024x1024", (8, 1024, 1024), "bf16")]
     ratios = [10, 100, 1000] if len(sys.argv) < 2 else [float(r) for r in sys.argv[1].split(",")]
+    if os.environ.get("GT_SHAPES"):  # comma-separated substrings of the shape names
+        keep = os.environ["GT_SHAPES"].split(",")
+        shapes = [s for s in shapes if any(k in s[0] for k in keep)]
     g = torch.Generator(device=dev).manual_seed(0)
     for name, shape, dt in shapes:
         x = torch.randn(shape, device=dev, generator=g).reshape(-1)
