@@ -53,6 +53,10 @@ namespace gp {
 
 constexpr int kMaxGridSpec = 160;      // largest grid: the one-round-trip FC gather stages G*32 keys in smem
 constexpr uint32_t kRing = 4;          // 1 KiB rows in flight per warp (bulk copies into smem)
+#ifndef GP_PREFETCH_ROWS
+#define GP_PREFETCH_ROWS 8
+#endif
+constexpr uint32_t kPrefetchRows = GP_PREFETCH_ROWS;  // further rows prefetched to L2 at kernel start
 
 // ---------------------------------------------------------------------------
 // list entries: (global index, raw bits) — 8 B for 16/32-bit, 16 B for 64-bit
@@ -107,6 +111,15 @@ struct WarpList {
 // the loads of kScanDepth steps in flight (spilled entries live in L2/HBM: one
 // round trip per step would serialise the pass).  body(valid, idx, bits) runs
 // warp-wide.
+// development aid: GP_EXIT_AT=n ends the kernel after phase n (timing by differences)
+#ifndef GP_EXIT_AT
+#define GP_EXIT_AT 99
+#endif
+#define EXIT_AT(n) \
+  do {             \
+    if (GP_EXIT_AT == (n)) return; \
+  } while (0)
+
 #ifndef GP_SCAN_DEPTH
 #define GP_SCAN_DEPTH 4
 #endif
@@ -242,6 +255,12 @@ __device__ __forceinline__ unsigned long long globaltimer_ns() {
     }                                                                   \
   } while (0)
 
+// per-warp cycle stamps (lane 0): a.dbg[32768 + unit * 16 + slot]
+#define WSTAMP(slot)                                                                         \
+  do {                                                                                       \
+    if (a.dbg != nullptr && lane == 0) a.dbg[32768 + (size_t)unit * 16 + (slot)] = clock64(); \
+  } while (0)
+
 // ---------------------------------------------------------------------------
 // shared-memory layout (bytes)
 
@@ -312,8 +331,10 @@ __global__ void __launch_bounds__(kCompressThreads, 1) compress_kernel(const Com
   uint32_t* bar = &ctrl[kCtrlBar];
   // this CTA's histogram replica (kHistCopies replicas cut same-address atomic contention)
   uint32_t* hist = a.hist1 + (size_t)(c & (kHistCopies - 1)) * kFineBinsMax;
+  WSTAMP(0);
 
   STAMP(0);
+  if (GP_EXIT_AT == 10) return;
   if (a.header != nullptr && c == 0 && tid == 0) {
     a.header[0] = (unsigned long long)d;
     a.header[1] = (unsigned long long)k;
@@ -338,9 +359,22 @@ __global__ void __launch_bounds__(kCompressThreads, 1) compress_kernel(const Com
     for (uint32_t s = 0; s < kRing; ++s) mbar_init(mbar + s * 8u, 1u);
     fence_mbar_init();
     for (uint32_t r = 0; r < min(nrow, kRing); ++r) issue(r, r);
+    // the next rows go to L2 now, so a short unit is not a chain of HBM round trips
+    if (nrow > kRing && kPrefetchRows > 0) {
+      const uint32_t r1 = min(nrow, kRing + kPrefetchRows);
+      prefetch_l2_bulk(xw + (size_t)kRing * 256u, (min(nch, r1 * 32u) - kRing * 32u) * 32u);
+    }
   }
   __syncwarp();
 
+  if (GP_EXIT_AT == 11 || GP_EXIT_AT == 12) {
+    if (GP_EXIT_AT == 12)
+      for (uint32_t r = 0; r < min(nrow, kRing); ++r) mbar_wait(mbar + r * 8u, 0u);
+    else if (lane == 0)
+      for (uint32_t r = 0; r < min(nrow, kRing); ++r) mbar_wait(mbar + r * 8u, 0u);
+    __syncwarp();
+    return;
+  }
   // ---- stage 0: low watermark from this CTA's own first rows (no extra traffic)
   for (uint32_t i = tid; i < kCoarseBins; i += kCompressThreads) sh_coarse[i] = 0u;
   if (tid < 32) sh_res[tid] = 0u;
@@ -397,6 +431,7 @@ __global__ void __launch_bounds__(kCompressThreads, 1) compress_kernel(const Com
   const uint32_t top = min(nfine, ((cmax + 1u) << (FB - 12)) + (2u << (FB - Tr::kExpBits)));
 
   STAMP(1);
+  EXIT_AT(1);
   uint32_t L = 0;                              // this warp's candidate count
   uint32_t my_lobin = (uint32_t)(lo0 >> FS);   // lowest fine bin this CTA histograms
   uint32_t my_maxb = 0;                        // 1 + highest fine bin this CTA histogrammed
@@ -450,60 +485,105 @@ __global__ void __launch_bounds__(kCompressThreads, 1) compress_kernel(const Com
     };
     // one 1 KiB row from ring slot `so`: lane holds 16-byte pieces h*32+lane
     // (h = 0, 1), i.e. elements [h*32*EPS + lane*EPS, +EPS) of the row
-    auto process = [&](uint32_t r, uint32_t so) {
-      const uint32_t npieces = 2u * min(32u, nch - r * 32u);
-      uint32_t m[2];
+    // Rows r and r+1 (ring slots so0, so1) in one step: the four 512-byte
+    // sub-rows j = 2*row + h are tested together and placed with one packed
+    // scan, so a warp's per-row dependent chain (scan, append, histogram) is
+    // paid once per two rows.  Lane holds 16-byte piece h*32+lane of each row,
+    // i.e. elements [h*32*EPS + lane*EPS, +EPS).
+    auto process2 = [&](uint32_t r, uint32_t so0, uint32_t so1) {
+      uint32_t m[4];
 #pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        const uint32_t piece = h * 32u + lane;
+      for (int j = 0; j < 4; ++j) {
+        const uint32_t rr = r + (j >> 1);
+        const uint32_t piece = (j & 1) * 32u + lane;
         uint32_t mm = 0;
-        if (piece < npieces) {
-          const uint4 v = ld_shared_v4(so + piece * 16u);
+        if (rr < nrow && piece < 2u * min(32u, nch - rr * 32u)) {
+          const uint4 v = ld_shared_v4((j < 2 ? so0 : so1) + piece * 16u);
 #pragma unroll
           for (int e = 0; e < EPS; ++e)
             if (all || test(Tr::lane(v, e))) mm |= 1u << e;
         }
-        m[h] = mm;
+        m[j] = mm;
       }
-      const uint32_t packed = __popc(m[0]) | (__popc(m[1]) << 16);
-      if (__any_sync(kFull, packed)) {
-        const uint32_t incl = warp_incl_scan(packed);
-        const uint32_t excl = incl - packed, tot = __shfl_sync(kFull, incl, 31);
-        const uint32_t from = L;
-        uint32_t pos[2] = {L + (excl & 0xFFFFu), L + (tot & 0xFFFFu) + (excl >> 16)};
-        L += (tot & 0xFFFFu) + (tot >> 16);
-        // append (divergent): each candidate is one LDS from the ring slot
+      const uint64_t packed = (uint64_t)__popc(m[0]) | ((uint64_t)__popc(m[1]) << 16) |
+                              ((uint64_t)__popc(m[2]) << 32) | ((uint64_t)__popc(m[3]) << 48);
+      // sparse step (the common case above r ~ 50): no lane holds two
+      // candidates in one sub-row, so ballots give every position directly and
+      // each candidate is histogrammed where it is appended
+      const uint32_t two = (m[0] & (m[0] - 1)) | (m[1] & (m[1] - 1)) | (m[2] & (m[2] - 1)) | (m[3] & (m[3] - 1));
+      if (!__any_sync(kFull, two)) {
+        const uint32_t lt = lanemask_lt();
 #pragma unroll
-        for (int h = 0; h < 2; ++h) {
-          uint32_t mm = m[h];
-          const uint32_t piece = h * 32u + lane;
-          const uint32_t base = u0 + r * (32u * EPL) + piece * EPS;
-          const uint32_t src = so + piece * 16u;
+        for (int j = 0; j < 4; ++j) {
+          const uint32_t bj = __ballot_sync(kFull, m[j] != 0u);
+          if (m[j]) {
+            const uint32_t e = __ffs(m[j]) - 1;
+            const uint32_t piece = (j & 1) * 32u + lane;
+            const Bits bv = ld_shared_elem<Tr>((j < 2 ? so0 : so1) + piece * 16u + e * (uint32_t)sizeof(Elem));
+            list.put(L + __popc(bj & lt), u0 + (r + (j >> 1)) * (32u * EPL) + piece * EPS + e, bv);
+            if (L + __popc(bj & lt) < kCap) count(bv);  // spilled entries are counted after the loop
+          }
+          L += __popc(bj);
+        }
+        return;
+      }
+      if (__any_sync(kFull, packed != 0)) {
+        const uint64_t incl = warp_incl_scan64(packed);
+        const uint64_t excl = incl - packed, tot = __shfl_sync(kFull, incl, 31);
+        const uint32_t from = L;
+        uint32_t pos[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          pos[j] = L + ((uint32_t)(excl >> (16 * j)) & 0xFFFFu);
+        }
+        {  // every earlier sub-row's total precedes sub-row j
+          uint32_t run = 0;
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            pos[j] += run;
+            run += (uint32_t)(tot >> (16 * j)) & 0xFFFFu;
+          }
+          L += run;
+        }
+        // append (divergent): each candidate is one LDS from its ring slot
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          uint32_t mm = m[j];
+          const uint32_t piece = (j & 1) * 32u + lane;
+          const uint32_t base = u0 + (r + (j >> 1)) * (32u * EPL) + piece * EPS;
+          const uint32_t src = (j < 2 ? so0 : so1) + piece * 16u;
           while (mm) {
             const uint32_t e = __ffs(mm) - 1;
             mm &= mm - 1;
-            list.put(pos[h]++, base + e, ld_shared_elem<Tr>(src + e * (uint32_t)sizeof(Elem)));
+            list.put(pos[j]++, base + e, ld_shared_elem<Tr>(src + e * (uint32_t)sizeof(Elem)));
           }
         }
         count_new(from);
       }
     };
+    static_assert(kRing % 2 == 0, "rows are consumed in pairs");
     const uint32_t q0 = seq;
     if (!preloaded && lane == 0) {
       fence_proxy_async_smem();
       for (uint32_t r = 0; r < min(nrow, kRing); ++r) issue(r, q0 + r);
     }
-    for (uint32_t r = 0; r < nrow; ++r) {
-      const uint32_t q = q0 + r, slot = q % kRing;
-      mbar_wait(mbar + slot * 8u, (q / kRing) & 1u);
-      process(r, ring + slot * 1024u);
+    for (uint32_t r = 0; r < nrow; r += 2) {
+      const uint32_t q = q0 + r, s0 = q % kRing, s1 = (q + 1) % kRing;
+      mbar_wait(mbar + s0 * 8u, (q / kRing) & 1u);
+      if (r + 1 < nrow) mbar_wait(mbar + s1 * 8u, ((q + 1) / kRing) & 1u);
+      if (r < 12 && preloaded) WSTAMP(2 + r);
+#ifndef GP_EXP_NOPROCESS
+      process2(r, ring + s0 * 1024u, ring + s1 * 1024u);
+#endif
       __syncwarp();
-      if (lane == 0 && r + kRing < nrow) {  // refill the slot just consumed
+      if (lane == 0 && r + kRing < nrow) {  // refill the two slots just consumed
         fence_proxy_async_smem();
         issue(r + kRing, q + kRing);
+        if (r + kRing + 1 < nrow) issue(r + kRing + 1, q + kRing + 1);
       }
     }
     seq = q0 + nrow;
+    if (preloaded) WSTAMP(14);
     const Key span = lo ? Tr::kInfAbs - lo_m1 : ~(Key)0;
     for (uint32_t i0 = nch * EPL; i0 < n; i0 += 32u) {  // scalar tail / unaligned input
       const uint32_t i = i0 + lane;
@@ -526,6 +606,7 @@ __global__ void __launch_bounds__(kCompressThreads, 1) compress_kernel(const Com
       if (L) atomicAdd(&sh_res[20], L);
     }
     __syncthreads();
+    if (preloaded) WSTAMP(15);
     my_maxb = max(my_maxb, sh_res[18]);
     for (uint32_t i = tid; i < kWinBins; i += kCompressThreads) {
       const uint32_t v = sh_win[i];
@@ -597,8 +678,10 @@ __global__ void __launch_bounds__(kCompressThreads, 1) compress_kernel(const Com
         }
       }
       if (pass == 0) STAMP(2);
+      EXIT_AT(2);
       grid_barrier(bar, G);  // ---- B1 (and the rescan barrier)
       if (pass == 0) STAMP(3);
+      EXIT_AT(3);
       const bool found = (pass == 1 || ctrl[kCtrlCands] >= k) && find_b1();
       if (pass == 1 || (found && ctrl[kCtrlMaxLoBin] - 1u <= B1)) break;
       lo = (Key)(found ? B1 : 0u) << FS;
@@ -606,6 +689,7 @@ __global__ void __launch_bounds__(kCompressThreads, 1) compress_kernel(const Com
     }
   }
   STAMP(4);
+  EXIT_AT(4);
 
   // bf16: the bits below the fine bin are constant, so B1 already is the key
   // (except bin 0, which holds both NaN, key 0, and +-0, key 1)
@@ -681,102 +765,67 @@ __global__ void __launch_bounds__(kCompressThreads, 1) compress_kernel(const Com
       fcreg[1] = (Key)sh_res[9];
     }
     STAMP(5);
+    EXIT_AT(5);
     grid_barrier(bar, G);  // ---- B2
     STAMP(6);
+    EXIT_AT(6);
 
-    // ---- stage 3: one round trip for every CTA's counts + first kSpec-2 FC keys
+    // ---- stage 3: one round trip for every CTA's window [sure count, FC
+    // count, first kSpec-2 FC keys]; warp w handles CTAs w, w+32, ... with
+    // lane j holding word j, so per-CTA sums are warp reductions.
     constexpr uint32_t kSpec = 32;
+    static_assert(kSpec == 32, "one CTA window per warp");
+    constexpr int R = (kMaxGridSpec + 31) / 32;
     Key* stage = reinterpret_cast<Key*>(smem + SL::coarse);  // coarse + window smem, free after stage 1
     static_assert(kMaxGridSpec * kSpec * sizeof(Key) <= (kCoarseBins + kWinBins) * 4, "staging fits");
+    const Key* fcall = reinterpret_cast<const Key*>(a.fcreg);
+    if (tid < 256) {
+      sh_lvl[tid] = 0u;  // radix digit histograms (two levels, alternating)
+      sh_low[tid] = 0u;
+    }
+    if (tid < 2) sh_res[24 + tid] = 0u;
     {
-      constexpr int R = (kMaxGridSpec * kSpec + kCompressThreads - 1) / kCompressThreads;
       Key v[R];
 #pragma unroll
       for (int r = 0; r < R; ++r) {
-        const uint32_t s = tid + r * kCompressThreads;
-        if (s < G * kSpec) v[r] = reinterpret_cast<const Key*>(a.fcreg)[(size_t)(s / kSpec) * kFcCap + s % kSpec];
+        const uint32_t c2 = w + 32u * r;
+        if (c2 < G) v[r] = fcall[(size_t)c2 * kFcCap + lane];
       }
 #pragma unroll
       for (int r = 0; r < R; ++r) {
-        const uint32_t s = tid + r * kCompressThreads;
-        if (s < G * kSpec) stage[s] = v[r];
+        const uint32_t c2 = w + 32u * r;
+        if (c2 < G) stage[c2 * kSpec + lane] = v[r];
       }
     }
     __syncthreads();
-    if (w == 0) {  // per-CTA prefixes of the sure and FC counts
-      const uint32_t per = (G + 31) / 32;
-      uint32_t sa = 0, sb = 0;
-      for (uint32_t i = 0; i < per; ++i) {
-        const uint32_t c2 = lane * per + i;
-        if (c2 < G) {
-          sa += (uint32_t)stage[c2 * kSpec];
-          sb += (uint32_t)stage[c2 * kSpec + 1];
-        }
-      }
-      const uint32_t ia = warp_incl_scan(sa), ib = warp_incl_scan(sb);
-      uint32_t ra = ia - sa, rb = ib - sb;
-      for (uint32_t i = 0; i < per; ++i) {
-        const uint32_t c2 = lane * per + i;
-        if (c2 < G) {
-          if (c2 == c) sh_res[10] = ra;
-          sh_fcoff[c2] = rb;
-          ra += (uint32_t)stage[c2 * kSpec];
-          rb += (uint32_t)stage[c2 * kSpec + 1];
-        }
-      }
-      if (lane == 31) sh_fcoff[G] = ib;
-    }
-    __syncthreads();
-    const uint32_t Mt = sh_fcoff[G];
-    const uint32_t sure_off = sh_res[10];
+    // every FC key of every CTA: the staged window, then (rare) the rest of a
+    // CTA holding more than kSpec-2; fn(c2, key) runs on this warp's lanes
+    auto for_fc_keys = [&](uint32_t c2, auto&& fn) {
+      const uint32_t cnt = (uint32_t)stage[c2 * kSpec + 1];
+      if (lane >= 2 && lane - 2 < cnt) fn(stage[c2 * kSpec + lane]);
+      for (uint32_t j = kSpec - 2 + lane; j < cnt; j += 32u) fn(fcall[(size_t)c2 * kFcCap + 2 + j]);
+    };
     uint32_t need = k - G1;
     Key T = (Key)B1 << FS;
     if (kDirectT) {
       T |= 1;  // every FC key equals T; the tie quota is the whole need
     } else {
-      // place the index-ordered FC list: position p belongs to the last CTA
-      // whose offset is <= p; ranks beyond the staged kSpec-2 keys take one
-      // more (independent) load, so a big FC list costs one extra round trip
-      {
-        constexpr int PER = kFcCap / kCompressThreads;
-        const Key* fcall = reinterpret_cast<const Key*>(a.fcreg);
-        Key v[PER];
-#pragma unroll
-        for (int i = 0; i < PER; ++i) {
-          const uint32_t p = tid + i * kCompressThreads;
-          v[i] = 0;
-          if (p < Mt) {
-            uint32_t lo = 0, hi = G;  // sh_fcoff[lo] <= p < sh_fcoff[hi]
-            while (hi - lo > 1u) {
-              const uint32_t mid = (lo + hi) >> 1;
-              if (sh_fcoff[mid] <= p) lo = mid;
-              else hi = mid;
-            }
-            const uint32_t j = p - sh_fcoff[lo];
-            v[i] = j < kSpec - 2 ? stage[lo * kSpec + 2 + j] : fcall[(size_t)lo * kFcCap + 2 + j];
-          }
-        }
-#pragma unroll
-        for (int i = 0; i < PER; ++i) {
-          const uint32_t p = tid + i * kCompressThreads;
-          if (p < Mt) sh_fckey[p] = v[i];
-        }
-      }
-      __syncthreads();
-      // in-smem radix select over the low FS bits of the final candidates
-      for (int hib = FS; hib > 0;) {
+      // radix select over the low FS bits of the (unordered) final candidates
+      for (int hib = FS, li = 0; hib > 0; ++li) {
         const int nb = hib < 8 ? hib : 8;
         const int lob = hib - nb;
-        if (tid < 256) sh_lvl[tid] = 0u;
-        __syncthreads();
-        for (uint32_t p = tid; p < Mt; p += kCompressThreads) {
-          const Key kk = sh_fckey[p];
-          if ((kk >> hib) == (T >> hib)) atomicAdd(&sh_lvl[(uint32_t)(kk >> lob) & ((1u << nb) - 1u)], 1u);
+        uint32_t* H = (li & 1) ? sh_low : sh_lvl;
+        for (int r = 0; r < R; ++r) {
+          const uint32_t c2 = w + 32u * r;
+          if (c2 < G)
+            for_fc_keys(c2, [&](Key kk) {
+              if ((kk >> hib) == (T >> hib)) atomicAdd(&H[(uint32_t)(kk >> lob) & ((1u << nb) - 1u)], 1u);
+            });
         }
         __syncthreads();
         if (w == 0) {
           uint32_t dig = 0, above = 0;
-          warp_cross_desc(sh_lvl, (1 << nb) - 1, need, &dig, &above);
+          warp_cross_desc(H, (1 << nb) - 1, need, &dig, &above);
           if (lane == 0) {
             sh_res[12] = dig;
             sh_res[13] = above;
@@ -786,53 +835,72 @@ __global__ void __launch_bounds__(kCompressThreads, 1) compress_kernel(const Com
         T |= (Key)sh_res[12] << lob;
         need -= sh_res[13];
         hib = lob;
+        if (tid < 256) H[tid] = 0u;  // reused two levels on, after at least one more barrier
       }
     }
     const uint32_t need_eq = need;  // number of key == T final candidates kept
     STAMP(7);
-    if (!kDirectT) {
-      constexpr int PER = kFcCap / kCompressThreads;
-      uint32_t pk[PER], s = 0;
-#pragma unroll
-      for (int b = 0; b < PER; ++b) {
-        const uint32_t p = PER * tid + b;
-        uint32_t v = 0;
-        if (p < Mt) {
-          const Key kk = sh_fckey[p];
-          v = (kk > T ? 0x10000u : 0u) | (kk == T ? 1u : 0u);
+    EXIT_AT(7);
+    // CTAs before this one: sure + (key > T) counts, and (key == T) counts;
+    // this CTA's own FC keys (index order): per-position (gt, eq) prefix
+    {
+      uint32_t acc_a = 0, acc_e = 0;
+      for (int r = 0; r < R; ++r) {
+        const uint32_t c2 = w + 32u * r;
+        if (c2 >= G || c2 > c) break;
+        const uint32_t cnt = (uint32_t)stage[c2 * kSpec + 1];
+        if (c2 < c) {
+          uint32_t gt = 0, eq = 0;
+          if (kDirectT) {
+            eq = lane == 0 ? cnt : 0u;
+          } else {
+            for_fc_keys(c2, [&](Key kk) {
+              gt += kk > T;
+              eq += kk == T;
+            });
+          }
+          acc_a += (lane == 0 ? (uint32_t)stage[c2 * kSpec] : 0u) + gt;
+          acc_e += eq;
+        } else {  // own CTA: sh_fcpre[i] = (gt << 16) | eq over own keys before i
+          uint32_t run = 0;
+          for (uint32_t j0 = 0; j0 < cnt; j0 += 32u) {
+            const uint32_t i = j0 + lane;
+            Key kk = T;
+            if (i < cnt && !kDirectT)
+              kk = i < kSpec - 2 ? stage[c2 * kSpec + 2 + i] : fcall[(size_t)c2 * kFcCap + 2 + i];
+            const bool valid = i < cnt;
+            const uint32_t v = valid ? ((kk > T ? 0x10000u : 0u) | (kk == T ? 1u : 0u)) : 0u;
+            const uint32_t incl = warp_incl_scan(v);
+            if (valid) sh_fcpre[i] = run + incl - v;
+            run += __shfl_sync(kFull, incl, 31);
+          }
+          if (lane == 0) sh_fcpre[cnt] = run;
         }
-        pk[b] = v;
-        s += v;
       }
-      uint32_t tot;
-      uint32_t run = block_excl_scan(s, sh32, &tot);
-#pragma unroll
-      for (int b = 0; b < PER; ++b) {
-        sh_fcpre[PER * tid + b] = run;
-        run += pk[b];
+      acc_a = warp_sum(acc_a);
+      acc_e = warp_sum(acc_e);
+      if (lane == 0) {
+        if (acc_a) atomicAdd(&sh_res[24], acc_a);
+        if (acc_e) atomicAdd(&sh_res[25], acc_e);
       }
-      if (tid == 0) sh_fcpre[kFcCap] = tot;
-      __syncthreads();
     }
-    // kept final candidates before FC position p
+    __syncthreads();
+    const uint32_t eq_before = sh_res[25];  // key == T final candidates in earlier CTAs
+    const uint32_t kept_eq0 = min(eq_before, need_eq);
+    // kept own final candidates before own FC position p
     auto fcsel = [&](uint32_t p) {
-      if (kDirectT) return min(p, need_eq);
       const uint32_t v = sh_fcpre[p];
-      return (v >> 16) + min(v & 0xFFFFu, need_eq);
+      return (v >> 16) + min(eq_before + (v & 0xFFFFu), need_eq) - kept_eq0;
     };
-    const uint32_t fc_c = sh_fcoff[c];
-    const uint32_t fcw = fc_c + w_boff[w];
-    uint32_t o = sure_off + fcsel(fc_c) + w_aoff[w] + (fcsel(fcw) - fcsel(fc_c));
-    uint32_t jfc = fcw;
+    uint32_t o = sh_res[24] + kept_eq0 + w_aoff[w] + fcsel(w_boff[w]);
+    uint32_t jfc = w_boff[w];
     list_scan<Tr>(list, L, [&](bool valid, uint32_t idx, Bits b) {
       const Key kk = Tr::key(b);
       const uint32_t fb = (uint32_t)(kk >> FS);
       const bool isfc = valid && fb == B1;
       const uint32_t fm = __ballot_sync(kFull, isfc);
       const uint32_t p = jfc + __popc(fm & lanemask_lt());
-      bool keep_fc;
-      if (kDirectT) keep_fc = p < need_eq;
-      else keep_fc = kk > T || (kk == T && (sh_fcpre[p] & 0xFFFFu) < need_eq);
+      const bool keep_fc = kk > T || (kk == T && eq_before + (sh_fcpre[p] & 0xFFFFu) < need_eq);
       const bool sel = valid && (fb > B1 || (isfc && keep_fc));
       const uint32_t sm = __ballot_sync(kFull, sel);
       if (sel) write_out<Tr>(a, o + __popc(sm & lanemask_lt()), idx, b);
@@ -933,6 +1001,7 @@ __global__ void __launch_bounds__(kCompressThreads, 1) compress_kernel(const Com
     }
   }
   STAMP(8);
+  EXIT_AT(8);
 
   // ---- leave the workspace clean: every bin this CTA added to its histogram
   // replica lies in [my_lobin, my_maxb); all histogram / control reads

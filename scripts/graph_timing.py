@@ -93,6 +93,10 @@ def main():
 
             t0 = graph_time([fl])
             t1 = graph_time([fl, comp])
+            if os.environ.get("GT_COMPRESS_ONLY"):  # exit-at-phase variants: no valid frame to decompress
+                tw = graph_time([comp])
+                print(f"{name:26s} r={r:6g} k={k:8d} | compress {t1 - t0:7.2f} us (warm {tw:6.2f})", flush=True)
+                continue
             t2 = graph_time([fl, comp, decomp])
             tw = graph_time([comp])
             twd = graph_time([decomp])

@@ -96,6 +96,13 @@ def main():
                 except ValueError:
                     pass
         print(f"== {k['name'][:100]}  ({fn}, {len(k['rows'])} instr, {total:.0f} samples)")
+        tot_st = defaultdict(float)
+        for d in agg.values():
+            for st, v in d.items():
+                if not st.startswith("_"):
+                    tot_st[st] += v
+        print("   stalls: " + ", ".join(f"{st}={100 * v / max(total, 1):.1f}%"
+                                       for st, v in sorted(tot_st.items(), key=lambda kv: -kv[1])[:10]))
         for loc, d in sorted(agg.items(), key=lambda kv: -kv[1]["_all"])[: args.top]:
             top = sorted(((s, v) for s, v in d.items() if not s.startswith("_")), key=lambda kv: -kv[1])[:3]
             print(f"  {loc[0]}:{loc[1]:<5d} {d['_all']:6.0f} ({100 * d['_all'] / max(total, 1):4.1f}%) "
