@@ -359,11 +359,9 @@ __global__ void __launch_bounds__(kCompressThreads, 1) compress_kernel(const Com
     for (uint32_t s = 0; s < kRing; ++s) mbar_init(mbar + s * 8u, 1u);
     fence_mbar_init();
     for (uint32_t r = 0; r < min(nrow, kRing); ++r) issue(r, r);
-    // the next rows go to L2 now, so a short unit is not a chain of HBM round trips
-    if (nrow > kRing && kPrefetchRows > 0) {
-      const uint32_t r1 = min(nrow, kRing + kPrefetchRows);
-      prefetch_l2_bulk(xw + (size_t)kRing * 256u, (min(nch, r1 * 32u) - kRing * 32u) * 32u);
-    }
+    // a short unit sends its remaining rows to L2 now (no second HBM round trip)
+    if (nrow > kRing && nrow <= kRing + kPrefetchRows)
+      prefetch_l2_bulk(xw + (size_t)kRing * 256u, (nch - kRing * 32u) * 32u);
   }
   __syncwarp();
 
@@ -375,58 +373,50 @@ __global__ void __launch_bounds__(kCompressThreads, 1) compress_kernel(const Com
     __syncwarp();
     return;
   }
-  // ---- stage 0: low watermark from this CTA's own first rows (no extra traffic)
+  // ---- stage 0: low watermark from a sample of this CTA's row 0s (no extra
+  // traffic): 4 elements per lane, one warp finds the crossing from the top
   for (uint32_t i = tid; i < kCoarseBins; i += kCompressThreads) sh_coarse[i] = 0u;
   if (tid < 32) sh_res[tid] = 0u;
   __syncthreads();
-  {
-    uint32_t ns = 0;
-    for (uint32_t r = 0; r < min(nrow, 2u); ++r) {
-      mbar_wait(mbar + r * 8u, 0u);
+  if (nrow > 0) {
+    mbar_wait(mbar, 0u);
+    WSTAMP(1);
+    uint32_t ns = 0, mb = 0;
 #pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        const uint32_t piece = h * 32u + lane;  // 16-byte piece of the row
-        if (piece < 2u * (nch - r * 32u)) {
-          const uint4 v = ld_shared_v4(ring + r * 1024u + piece * 16u);
-          atomicAdd(&sh_coarse[(uint32_t)(Tr::key(Tr::lane(v, 0)) >> CS)], 1u);
+    for (int h = 0; h < 2; ++h) {
+      const uint32_t piece = h * 32u + lane;  // 16-byte piece of row 0
+      if (piece < 2u * nch) {
+        const uint4 v = ld_shared_v4(ring + piece * 16u);
+#pragma unroll
+        for (int e = 0; e < EPS; e += EPS / 2) {
+          const uint32_t bin = (uint32_t)(Tr::key(Tr::lane(v, e)) >> CS);
+          atomicAdd(&sh_coarse[bin], 1u);
+          mb = max(mb, bin + 1u);
           ++ns;
         }
       }
     }
     ns = warp_sum(ns);
-    if (lane == 0 && ns) atomicAdd(&sh_res[19], ns);
+    mb = __reduce_max_sync(kFull, mb);
+    if (lane == 0 && ns) {
+      atomicAdd(&sh_res[19], ns);
+      atomicMax(&sh_res[16], mb);
+    }
   }
   __syncthreads();
-  Key lo0 = 0;
-  uint32_t cmax;  // highest non-empty coarse bin of the sample
-  {
+  if (w == 0 && sh_res[16]) {
     const uint32_t S = sh_res[19];
-    uint32_t v[4], m = 0, ts = 0;
-#pragma unroll
-    for (int b = 0; b < 4; ++b) {
-      v[b] = sh_coarse[4 * tid + b];
-      if (v[b]) m = 4 * tid + b + 1;
-      ts += v[b];
-    }
-    m = __reduce_max_sync(kFull, m);
-    if (lane == 0 && m) atomicMax(&sh_res[16], m);
     const double mu = (double)S * (double)k / (double)d;
     const double rs = ceil(mu + 4.0 * sqrt(mu) + 8.0);
-    uint32_t tot;
-    const uint32_t excl = block_excl_scan(ts, sh32, &tot);
     if (rs < (double)S) {
-      const uint32_t target = (uint32_t)rs;
-      uint32_t run = tot - excl - ts;  // sample count in bins above this thread's
-#pragma unroll
-      for (int b = 3; b >= 0; --b) {
-        if (run < target && run + v[b] >= target) sh_res[17] = 4 * tid + b + 1;
-        run += v[b];
-      }
+      uint32_t bin = 0, above = 0;
+      if (warp_cross_desc(sh_coarse, (int)sh_res[16] - 1, (uint32_t)rs, &bin, &above) && lane == 0)
+        sh_res[17] = bin + 1u;
     }
-    __syncthreads();
-    if (sh_res[17]) lo0 = (Key)(sh_res[17] - 1) << CS;
-    cmax = sh_res[16] ? sh_res[16] - 1 : (uint32_t)(kCoarseBins - 1);
   }
+  __syncthreads();
+  const Key lo0 = sh_res[17] ? (Key)(sh_res[17] - 1) << CS : (Key)0;
+  const uint32_t cmax = sh_res[16] ? sh_res[16] - 1 : (uint32_t)(kCoarseBins - 1);  // highest sampled coarse bin
   // top of the smem histogram window: two exponents above the sample maximum
   const uint32_t top = min(nfine, ((cmax + 1u) << (FB - 12)) + (2u << (FB - Tr::kExpBits)));
 

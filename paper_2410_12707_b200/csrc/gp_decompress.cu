@@ -31,6 +31,11 @@ constexpr int kDecThreads = 512;
 constexpr int kDecBlocksPerSm = 4;
 constexpr int kTileBytes = 16 * 1024;   // smem output tile (double-buffered)
 constexpr int64_t kMinChunk = 8192;
+#ifndef GP_SPARSE_DENSITY_INV
+#define GP_SPARSE_DENSITY_INV 20
+#endif
+constexpr int64_t kSparseDensityInv = GP_SPARSE_DENSITY_INV;  // fill+scatter when k/d <= 1/this
+constexpr int64_t kSparseMaxBytes = 64ll << 20;  // ... and the output fits well inside L2 (126 MB)
 
 // ---- value conversions (exact for f32<->f64 widening and bf16<->f32 of bf16 values)
 __device__ __forceinline__ float bf16_to_f32(uint16_t b) { return __uint_as_float((uint32_t)b << 16); }
@@ -248,6 +253,85 @@ __global__ void __launch_bounds__(kDecThreads, kDecBlocksPerSm) decompress_kerne
 #undef DSTAMP
 }
 
+// Sparse fast path (mode 0, k/d <= 1/20, output <= 64 MB): each CTA zero-fills
+// its output range with 128-bit stores straight away, overlapping the round
+// trips that locate its entries, then scatters those entries (after a CTA
+// barrier, so each value lands after the zero written to its address by a
+// sibling thread).  The output fits in L2, so the scattered sectors merge there
+// and HBM still sees every output line once; no smem staging, no per-tile
+// barriers.  (For larger outputs the fill evicts lines before the scatter and
+// the tiled kernel wins.)  Validation is the same as the tiled kernel's.
+template <class IT, class VT, class OT>
+__global__ void __launch_bounds__(kDecThreads, kDecBlocksPerSm) decompress_sparse_kernel(
+    const IT* __restrict__ idx, const VT* __restrict__ vals, int64_t k, int64_t d, int64_t chunk,
+    OT* __restrict__ out, uint32_t* err) {
+  const uint32_t tid = threadIdx.x;
+  const int64_t o0 = min((int64_t)blockIdx.x * chunk, d);
+  const int64_t o1 = min(o0 + chunk, d);
+  bool bad = false;
+  const int64_t P = k > 1 ? k - 1 : 0;
+  const int64_t pb = (P * (int64_t)blockIdx.x) / gridDim.x;
+  const int64_t pe = (P * ((int64_t)blockIdx.x + 1)) / gridDim.x;
+  int64_t pa = 0, pz = 1;
+  if (pb + tid < pe) {
+    pa = (int64_t)__ldg(idx + pb + tid);
+    pz = (int64_t)__ldg(idx + pb + tid + 1);
+  }
+  int64_t first = 0, last = 0;
+  if (blockIdx.x == 0 && tid == 0 && k > 0) {
+    first = (int64_t)__ldg(idx);
+    last = (int64_t)__ldg(idx + k - 1);
+  }
+  const int64_t guess = d ? (int64_t)((double)k * (double)o0 / (double)d) : 0;
+  const int64_t stride = max((int64_t)1, (int64_t)(3.0f * sqrtf((float)k) / kDecThreads) + 1);
+  auto probe_pos = [&](int64_t t) {
+    const int64_t p = guess + (t - kDecThreads / 2) * stride;
+    return p < 0 ? (int64_t)0 : (p >= k ? k - 1 : p);
+  };
+  int64_t pv = 0;
+  if (k > 0) pv = (int64_t)__ldg(idx + probe_pos(tid));
+  // zero fill of the whole range while the probes are in flight
+  if (((uintptr_t)(out + o0) % 16) == 0) {
+    constexpr int V = 16 / (int)sizeof(OT);
+    const int64_t nvec = (o1 - o0) / V;
+    uint4* ov = reinterpret_cast<uint4*>(out + o0);
+    for (int64_t i = tid; i < nvec; i += kDecThreads) ov[i] = make_uint4(0u, 0u, 0u, 0u);
+    for (int64_t i = o0 + nvec * V + tid; i < o1; i += kDecThreads) out[i] = OT(0);
+  } else {
+    for (int64_t i = o0 + tid; i < o1; i += kDecThreads) out[i] = OT(0);
+  }
+  if (k == 0) return;
+  if (!(pa < pz)) bad = true;
+  if (blockIdx.x == 0 && tid == 0 && (first < 0 || last >= d)) atomicOr(err, 1u);
+  __shared__ int64_t sh_lo;
+  const int below = __syncthreads_count(pv < o0);  // also orders the fill before the scatter
+  int64_t base;
+  const int64_t p_first = probe_pos(0), p_last = probe_pos(kDecThreads - 1);
+  if ((below == 0 && p_first > 0) || (below == kDecThreads && p_last < k - 1)) {
+    if (tid < 32) {  // probe window missed (clustered indices)
+      const int64_t r = warp_lower_bound(idx, k, o0, guess);
+      if ((tid & 31) == 0) sh_lo = r;
+    }
+    __syncthreads();
+    base = sh_lo;
+  } else {
+    base = below == 0 ? 0 : probe_pos(below - 1) + 1;  // lower_bound(o0) in [base, base + stride]
+  }
+  for (;; base += kDecThreads) {
+    const int64_t j = base + tid;
+    bool past = j >= k;
+    if (!past) {
+      const int64_t i = (int64_t)__ldg(idx + j);
+      if (i >= o1) past = true;
+      else if (i >= o0) out[i] = cvt<OT>(__ldg(vals + j));  // base may trail lower_bound(o0) by < stride
+    }
+    if (__syncthreads_or(past)) break;
+  }
+  for (int64_t j = pb + tid + kDecThreads; j < pe; j += kDecThreads)
+    if (!((int64_t)__ldg(idx + j) < (int64_t)__ldg(idx + j + 1))) bad = true;
+  if (__syncthreads_or(bad) && tid == 0) atomicOr(err, 2u);
+}
+
 // ---- general path
 template <class OT>
 __global__ void zero_kernel(OT* out, int64_t d) {
@@ -287,8 +371,13 @@ static int run_fast(const DecompressArgs& a, const DeviceInfo& dev, cudaStream_t
                          cudaSharedmemCarveoutMaxShared);
     carveout_set[dev.ordinal] = true;
   }
-  decompress_kernel<IT, VT, OT><<<(unsigned)grid, kDecThreads, 0, s>>>(
-      (const IT*)a.idx, (const VT*)a.vals, a.k, a.d, chunk, (OT*)a.out, a.mode, a.err, a.dbg);
+  if (a.mode == 0 && a.k * kSparseDensityInv <= a.d && a.d * (int64_t)sizeof(OT) <= kSparseMaxBytes) {
+    decompress_sparse_kernel<IT, VT, OT><<<(unsigned)grid, kDecThreads, 0, s>>>(
+        (const IT*)a.idx, (const VT*)a.vals, a.k, a.d, chunk, (OT*)a.out, a.err);
+  } else {
+    decompress_kernel<IT, VT, OT><<<(unsigned)grid, kDecThreads, 0, s>>>(
+        (const IT*)a.idx, (const VT*)a.vals, a.k, a.d, chunk, (OT*)a.out, a.mode, a.err, a.dbg);
+  }
   return cudaGetLastError() == cudaSuccess ? 0 : 5;
 }
 

@@ -7,11 +7,11 @@ from pathlib import Path
 
 ROOT = Path(__file__).resolve().parent.parent
 SRC = ROOT / "paper_2410_12707_b200" / "csrc" / "gp_compress.cu"
-MARKERS = [("prologue+watermark", "template <class Tr>\n__global__ void __launch_bounds__(kCompressThreads, 1) compress_kernel"),
+MARKERS = [("prologue+watermark", "compress_kernel(const CompressArgs a) {"),
            ("stream", "  auto stream_unit = [&]"), ("find", "  auto find_b1 = [&]"),
            ("pass loop/B1", "  // first pass, and at most one partial rescan"),
            ("split", "    // One pass over the list: per-warp sure"),
-           ("fc-resolve", "    // ---- stage 3: one round trip"), ("walk", "    // kept final candidates before FC"),
+           ("fc-resolve", "    // ---- stage 3: one round trip"), ("walk", "    uint32_t jfc = w_boff[w];"),
            ("slow path", "    // ================= slow path"), ("cleanup", "  // ---- leave the workspace clean")]
 
 

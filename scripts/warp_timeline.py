@@ -52,7 +52,7 @@ def main():
     w = a[32768:32768 + G * 32 * 16].reshape(G * 32, 16).astype(np.float64)
     base = w[:, 0:1]
     rel = (w - base) / f / 1e3  # us since the warp's start
-    names = ["start", "watermark"] + [f"row{r}" for r in range(12)] + ["loop end", "flushed"]
+    names = ["start", "row0 in"] + [f"row{r}" for r in range(12)] + ["loop end", "flushed"]
     print(f"d={d} k={k} G={G} clock {f:.3f} GHz; per-warp us since warp start (mean / p90 / max)")
     for i, nm in enumerate(names):
         col = rel[:, i][w[:, i] > 0]

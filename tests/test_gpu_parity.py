@@ -396,3 +396,29 @@ def test_host_pinned_input_e2e(cuda):
     p = P.topk_compress(x, 100)
     vals, idx, d = O.topk_compress(x.numpy(), 100, method="threshold")
     np.testing.assert_array_equal(p.indices.cpu().numpy(), idx)
+
+
+@pytest.mark.parametrize("ratio", [3, 10, 30, 100, 1000, 20000])
+def test_decompress_frame_large_k_both_kernels(cuda, ratio):
+    """Both fast decompress kernels (tiled, dense payloads; fill+scatter, sparse
+    payloads) at k large enough that the probe bracket is wider than one entry:
+    no spurious error flag, and the output equals x on the support, 0 elsewhere."""
+    L = _lib.lib()
+    g = torch.Generator(device=cuda).manual_seed(ratio)
+    x = torch.randn(12_845_056, device=cuda, generator=g)
+    d = x.numel()
+    k = P.select_k(d, ratio)
+    s = torch.cuda.current_stream().cuda_stream
+    frame = torch.empty(16 + 12 * k, dtype=torch.uint8, device=cuda)
+    wsb = L.gp_topk_workspace_bytes(d, _lib.DTYPE_F32)
+    ws = torch.empty(wsb, dtype=torch.uint8, device=cuda)
+    assert L.gp_workspace_init(ws.data_ptr(), wsb, s) == 0
+    assert L.gp_topk_compress_frame(x.data_ptr(), 0, d, k, frame.data_ptr(), ws.data_ptr(), wsb, s) == 0
+    out = torch.full((d,), float("nan"), device=cuda)
+    err = torch.zeros(1, dtype=torch.int32, device=cuda)
+    assert L.gp_topk_decompress_frame(frame.data_ptr(), k, d, out.data_ptr(), 0, 0, err.data_ptr(), s) == 0
+    assert int(err.item()) == 0
+    idx = frame[16:16 + 8 * k].view(torch.int64)
+    ref = torch.zeros_like(x)
+    ref[idx] = x[idx]
+    assert torch.equal(out, ref)
