@@ -31,7 +31,7 @@ def main(src, md_out, json_out):
         names[int(r[0])] = r[4]
     ids = sorted(launches)
     comp = [i for i in ids if names[i].startswith("void compress_kernel")]
-    dec = [i for i in ids if "decompress_kernel" in names[i]]
+    dec = [i for i in ids if "decompress" in names[i]]
     us = list(units())
     lines = ["| unit | kernel | time us | DRAM read MB | DRAM write MB | algorithmic MB | DRAM/alg |",
              "|---|---|---|---|---|---|---|"]
