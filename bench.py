@@ -189,14 +189,14 @@ def run_ours(args, rank, world, local_rank):
     flush = torch.ones(128 << 20, dtype=torch.float32, device=dev)  # 512 MB read between steps
     step_bytes = sum(pair_bytes(u["d"], 4, u["k"]) for u in units)
 
-    def compress(u):
+    def compress(u):  # on the current stream (the capture stream while a graph is recorded)
         st = L.gp_topk_compress_frame(u["x"].data_ptr(), 0, u["d"], u["k"], u["frame"].data_ptr(), ws.data_ptr(),
-                                      wsb, sp)
+                                      wsb, torch.cuda.current_stream(dev).cuda_stream)
         assert st == 0, st
 
     def decompress(u, frame):
         st = L.gp_topk_decompress_frame(frame.data_ptr(), u["k"], u["d"], u["out"].data_ptr(), 0, 0,
-                                        err.data_ptr(), sp)
+                                        err.data_ptr(), torch.cuda.current_stream(dev).cuda_stream)
         assert st == 0, st
 
     def exchange():
@@ -208,21 +208,55 @@ def run_ours(args, rank, world, local_rank):
         for w in dist.batch_isend_irecv(ops):
             w.wait()
 
-    def step(ev=None):
+    def compress_all(ev=None):
         for i, u in enumerate(units):
             if ev is not None:
                 ev[i][0].record(stream)
             compress(u)
             if ev is not None:
                 ev[i][1].record(stream)
-        if world > 1:
-            exchange()
+
+    def decompress_all(ev=None):
         for i, u in enumerate(units):
             if ev is not None:
                 ev[i][2].record(stream)
             decompress(u, u["rframe"] if world > 1 else u["frame"])
             if ev is not None:
                 ev[i][3].record(stream)
+
+    def step(ev=None):
+        compress_all(ev)
+        if world > 1:
+            exchange()
+        decompress_all(ev)
+
+    # The timed step replays two CUDA graphs (all compress launches, then all
+    # decompress launches; the NCCL frame exchange runs eagerly in between at
+    # N>1): launch-bound sequences of 24 kernels are what graphs are for.
+    graphs = None
+    if not args.no_graph:
+        side = torch.cuda.Stream(dev)
+        side.wait_stream(stream)
+        with torch.cuda.stream(side):
+            step()  # warm the launch path on the capture stream
+        stream.wait_stream(side)
+        torch.cuda.synchronize(dev)
+        graphs = []
+        for fn in (compress_all, decompress_all):
+            gph = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(gph, stream=side):
+                fn()
+            graphs.append(gph)
+        torch.cuda.synchronize(dev)
+
+    def timed_step():
+        if graphs is None:
+            step()
+            return
+        graphs[0].replay()
+        if world > 1:
+            exchange()
+        graphs[1].replay()
 
     def barrier():
         if world > 1:
@@ -247,22 +281,33 @@ def run_ours(args, rank, world, local_rank):
     barrier()
     assert int(err.item()) == 0
 
-    # ---- timed region
+    # ---- timed region: whole steps only (no per-launch events inside)
     mk = lambda: torch.cuda.Event(enable_timing=True)  # noqa: E731
+    for _ in range(args.warmup):
+        timed_step()
+    barrier()
     step_ms, comp_us, decomp_us = [], [], []
     for _ in range(args.steps):
         flush.sum()  # L2 flush (outside the events)
         barrier()
         s0, s1 = mk(), mk()
-        ev = [[mk() for _ in range(4)] for _ in units]
         s0.record(stream)
-        step(ev)
+        timed_step()
         s1.record(stream)
         barrier()
         step_ms.append(s0.elapsed_time(s1))
+    clk = clocks.stop()
+    assert int(err.item()) == 0, "decompress validation flag raised"
+    # per-launch kernel times (roofline, per_config): separate eager steps with
+    # an event pair around every launch, same flush discipline
+    for _ in range(max(3, min(args.steps, 5))):
+        flush.sum()
+        barrier()
+        ev = [[mk() for _ in range(4)] for _ in units]
+        step(ev)
+        barrier()
         comp_us.append([e[0].elapsed_time(e[1]) * 1e3 for e in ev])
         decomp_us.append([e[2].elapsed_time(e[3]) * 1e3 for e in ev])
-    clk = clocks.stop()
     assert int(err.item()) == 0, "decompress validation flag raised"
 
     t_step = statistics.mean(step_ms)
@@ -300,6 +345,9 @@ def run_ours(args, rank, world, local_rank):
         "config": {"workload": WORKLOAD, "shapes": [list(s) for s in SHAPES], "ratios": RATIOS,
                    "pairs_per_step": len(units), "bytes_per_step_per_rank": step_bytes,
                    "l2": "512 MB read flush between timed steps; each step reads 771 MB of inputs (> L2)",
+                   "launch": ("eager launches" if args.no_graph else
+                              "2 CUDA graph replays per step (24 compress, then 24 decompress launches)"),
+                   "kernel_times": "per-launch CUDA events from separate eager steps (roofline, per_config)",
                    "parallelism": ("replicas, no exchange" if world == 1 else
                                    f"{world} ranks, compressed frames ring-exchanged over NCCL P2P (batch_isend_irecv)")},
         "roofline": {"bound": "hbm", "kernel": "compress_kernel<f32> (cooperative, 1 CTA/SM)",
@@ -426,17 +474,24 @@ def bench_e2e(P, dev, steps=2):
             base = torch.randn(shape, generator=g)
             x = (torch.relu(base) if kind == "activation" else base * 1e-3).reshape(-1).contiguous().pin_memory()
             hosts.append(x)
-    outs = [torch.empty_like(h).pin_memory() for h in hosts]
+    outs = [[torch.empty_like(h).pin_memory() for _ in RATIOS] for h in hosts]
+    # Pairs alternate between two streams, so one pair's D2H read overlaps the
+    # next pair's H2D upload (PCIe is full duplex); every call is the public
+    # drop-in API, each on the caller's current stream.
+    streams = [torch.cuda.Stream(dev) for _ in range(int(os.environ.get("GP_E2E_STREAMS", "2")))]
     total_bytes, h2d, d2h = 0, 0, 0
     times = []
     for s in range(steps + 1):
         torch.cuda.synchronize(dev)
         t0 = time.perf_counter()
-        for h, o in zip(hosts, outs):
-            for r in RATIOS:
-                p = P.topk_compress(h, r)          # H2D of the pinned input inside
-                dense = P.topk_decompress(p)       # device result
-                o.copy_(dense)                     # D2H of the result
+        n = 0
+        for h, os_ in zip(hosts, outs):
+            for r, o in zip(RATIOS, os_):
+                with torch.cuda.stream(streams[n % len(streams)]):
+                    p = P.topk_compress(h, r)          # H2D of the pinned input inside
+                    dense = P.topk_decompress(p)       # device result (validation flag read back)
+                    o.copy_(dense, non_blocking=True)  # D2H of the result
+                n += 1
                 if s == 0:
                     total_bytes += pair_bytes(h.numel(), 4, p.k)
                     h2d += h.numel() * 4
@@ -447,7 +502,8 @@ def bench_e2e(P, dev, steps=2):
     t = statistics.mean(times)
     return {"value": round(total_bytes / t / 1e9, 2), "unit": "GB/s", "h2d_bytes_per_step": h2d,
             "d2h_bytes_per_step": d2h, "ms_per_step": round(t * 1e3, 2),
-            "api": "paper_2410_12707_b200.topk_compress / topk_decompress (drop-in for geopipe.compressor)"}
+            "api": "paper_2410_12707_b200.topk_compress / topk_decompress (drop-in for geopipe.compressor), "
+                   "pairs alternating over 2 streams"}
 
 
 def main():
@@ -455,6 +511,7 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--no-graph", action="store_true", help="timed steps as eager launches (no CUDA graphs)")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-pipeline", action="store_true", help="skip the GPT-2 pipeline sub-measurement")
     args = ap.parse_args()
