@@ -104,6 +104,8 @@ struct TraitsF64 {
 // ---------------------------------------------------------------------------
 // warp / memory primitives
 
+__device__ __forceinline__ uint32_t sub_sat(uint32_t a, uint32_t b) { return a > b ? a - b : 0u; }
+
 __device__ __forceinline__ uint32_t lanemask_lt() {
   uint32_t m;
   asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));

@@ -143,6 +143,45 @@ __device__ __forceinline__ void list_scan(const WarpList<Tr>& list, uint32_t L, 
   }
 }
 
+// Same, two consecutive entries per lane (one 16-byte load for 8-byte
+// entries): 64 entries per step, lane l holding entries 2l and 2l+1, so index
+// order is (lane, e) and positions come from two ballots, no scan.
+// body(v0, idx0, bits0, v1, idx1, bits1) runs warp-wide.
+template <class Tr, class F>
+__device__ __forceinline__ void list_scan2(const WarpList<Tr>& list, uint32_t L, F&& body) {
+  const uint32_t lane = threadIdx.x & 31;
+  constexpr uint32_t kCap = Entry<Tr>::kSmemCap;
+  static_assert(kCap % 2 == 0, "entry pairs never straddle smem/global");
+  for (uint32_t base = 0; base < L; base += kScanDepth * 64u) {
+    uint32_t idx[kScanDepth][2];
+    typename Tr::Bits b[kScanDepth][2];
+#pragma unroll
+    for (int q = 0; q < kScanDepth; ++q) {
+      const uint32_t j = base + q * 64u + 2u * lane;
+      idx[q][0] = idx[q][1] = 0;
+      b[q][0] = b[q][1] = 0;
+      if (j < L) {
+        const unsigned char* src = j < kCap ? list.smem : list.glob;
+        if constexpr (Entry<Tr>::kBytes == 8) {
+          const uint4 e = *reinterpret_cast<const uint4*>(src + (size_t)j * 8);
+          idx[q][0] = e.x;
+          b[q][0] = e.y;
+          idx[q][1] = e.z;
+          b[q][1] = e.w;
+        } else {
+          Entry<Tr>::get(src, j, idx[q][0], b[q][0]);
+          Entry<Tr>::get(src, j + 1, idx[q][1], b[q][1]);
+        }
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < kScanDepth; ++q) {
+      const uint32_t j = base + q * 64u + 2u * lane;
+      if (base + q * 64u < L) body(j < L, idx[q][0], b[q][0], j + 1 < L, idx[q][1], b[q][1]);
+    }
+  }
+}
+
 template <class Tr>
 __device__ __forceinline__ typename Tr::Bits load_bits(const void* x, uint32_t i) {
   return (typename Tr::Bits)__ldg(reinterpret_cast<const typename Tr::Elem*>(x) + i);
@@ -424,7 +463,6 @@ __global__ void __launch_bounds__(kCompressThreads, 1) compress_kernel(const Com
   EXIT_AT(1);
   uint32_t L = 0;                              // this warp's candidate count
   uint32_t my_lobin = (uint32_t)(lo0 >> FS);   // lowest fine bin this CTA histograms
-  uint32_t my_maxb = 0;                        // 1 + highest fine bin this CTA histogrammed
 
   // ---- stage 1 (and the rare rescan): stream the unit, keep keys >= lo and
   // histogram those whose fine bin is below add_below
@@ -597,7 +635,6 @@ __global__ void __launch_bounds__(kCompressThreads, 1) compress_kernel(const Com
     }
     __syncthreads();
     if (preloaded) WSTAMP(15);
-    my_maxb = max(my_maxb, sh_res[18]);
     for (uint32_t i = tid; i < kWinBins; i += kCompressThreads) {
       const uint32_t v = sh_win[i];
       if (v) red_add_gpu(&hist[wb + i], v);
@@ -612,9 +649,12 @@ __global__ void __launch_bounds__(kCompressThreads, 1) compress_kernel(const Com
   // ---- stage 2 helper: sum the replicas from the top, 4096 bins per step,
   // and find the fine bin holding the k-th largest key
   uint32_t B1 = 0, G1 = 0, M = 0;
+  uint32_t pop_lo = 0, pop_hi = 0;  // every populated bin of every replica lies in [pop_lo, pop_hi)
   auto find_b1 = [&]() -> bool {
     const uint32_t mb = ctrl[kCtrlMaxBin];
     const int lowest = (int)(0xFFFFFFFFu - ctrl[kCtrlMinLoBin]);  // no bin below any watermark is populated
+    pop_lo = (uint32_t)lowest;
+    pop_hi = mb;
     if (tid == 0) sh_res[0] = 0u;
     uint32_t base = 0;
     for (int t0 = (int)mb - 1; t0 >= lowest; t0 -= 4 * kCompressThreads) {
@@ -697,17 +737,19 @@ __global__ void __launch_bounds__(kCompressThreads, 1) compress_kernel(const Com
     Key* stagew = sh_fckey + w * kStageW;
     {
       uint32_t ca = 0, cb = 0;
-      list_scan<Tr>(list, L, [&](bool valid, uint32_t, Bits b) {
-        const Key kk = Tr::key(b);
-        const uint32_t fb = (uint32_t)(kk >> FS);
-        const bool isfc = valid && fb == B1;
-        const uint32_t fm = __ballot_sync(kFull, isfc);
-        ca += __popc(__ballot_sync(kFull, valid && fb > B1));
-        if (!kDirectT && isfc) {
-          const uint32_t p = cb + __popc(fm & lanemask_lt());
-          if (p < kStageW) stagew[p] = kk;
+      const uint32_t lt = lanemask_lt();
+      list_scan2<Tr>(list, L, [&](bool v0, uint32_t, Bits b0, bool v1, uint32_t, Bits b1) {
+        const Key k0 = Tr::key(b0), k1 = Tr::key(b1);
+        const uint32_t f0 = (uint32_t)(k0 >> FS), f1 = (uint32_t)(k1 >> FS);
+        const bool fc0 = v0 && f0 == B1, fc1 = v1 && f1 == B1;
+        const uint32_t m0 = __ballot_sync(kFull, fc0), m1 = __ballot_sync(kFull, fc1);
+        ca += __popc(__ballot_sync(kFull, v0 && f0 > B1)) + __popc(__ballot_sync(kFull, v1 && f1 > B1));
+        if (!kDirectT && (m0 | m1)) {
+          const uint32_t p0 = cb + __popc(m0 & lt) + __popc(m1 & lt);
+          if (fc0 && p0 < kStageW) stagew[p0] = k0;
+          if (fc1 && p0 + fc0 < kStageW) stagew[p0 + fc0] = k1;
         }
-        cb += __popc(fm);
+        cb += __popc(m0) + __popc(m1);
       });
       if (lane == 0) {
         w_a[w] = ca;
@@ -788,12 +830,60 @@ __global__ void __launch_bounds__(kCompressThreads, 1) compress_kernel(const Com
       }
     }
     __syncthreads();
-    // every FC key of every CTA: the staged window, then (rare) the rest of a
-    // CTA holding more than kSpec-2; fn(c2, key) runs on this warp's lanes
+    // Keys beyond the first kSpec-2 of a CTA (many FC keys, e.g. r = 10 on a
+    // large tensor) are fetched once, in one round trip, into sh_fckey
+    // (flattened; sh_fcoff[c2] = offset of CTA c2's extras, sh_fcoff[G] = total).
+    if (!kDirectT) {
+      if (w == 0) {
+        const uint32_t per = (G + 31) / 32;
+        uint32_t sx = 0;
+        for (uint32_t i = 0; i < per; ++i) {
+          const uint32_t c2 = lane * per + i;
+          if (c2 < G) sx += sub_sat((uint32_t)stage[c2 * kSpec + 1], kSpec - 2);
+        }
+        const uint32_t incl = warp_incl_scan(sx);
+        uint32_t run = incl - sx;
+        for (uint32_t i = 0; i < per; ++i) {
+          const uint32_t c2 = lane * per + i;
+          if (c2 < G) {
+            sh_fcoff[c2] = run;
+            run += sub_sat((uint32_t)stage[c2 * kSpec + 1], kSpec - 2);
+          }
+        }
+        if (lane == 31) sh_fcoff[G] = incl;
+      }
+      __syncthreads();
+      const uint32_t nx = sh_fcoff[G];
+      if (nx) {
+        constexpr int PER = kFcCap / kCompressThreads;
+        Key v[PER];
+#pragma unroll
+        for (int i = 0; i < PER; ++i) {
+          const uint32_t p = tid + i * kCompressThreads;
+          if (p < nx) {
+            uint32_t lo = 0, hi = G;  // sh_fcoff[lo] <= p < sh_fcoff[hi]
+            while (hi - lo > 1u) {
+              const uint32_t mid = (lo + hi) >> 1;
+              if (sh_fcoff[mid] <= p) lo = mid;
+              else hi = mid;
+            }
+            v[i] = fcall[(size_t)lo * kFcCap + kSpec + (p - sh_fcoff[lo])];
+          }
+        }
+#pragma unroll
+        for (int i = 0; i < PER; ++i) {
+          const uint32_t p = tid + i * kCompressThreads;
+          if (p < nx) sh_fckey[p] = v[i];
+        }
+        __syncthreads();
+      }
+    }
+    // every FC key of every CTA (staged window, then the CTA's extras);
+    // fn(key) runs on this warp's lanes
     auto for_fc_keys = [&](uint32_t c2, auto&& fn) {
       const uint32_t cnt = (uint32_t)stage[c2 * kSpec + 1];
       if (lane >= 2 && lane - 2 < cnt) fn(stage[c2 * kSpec + lane]);
-      for (uint32_t j = kSpec - 2 + lane; j < cnt; j += 32u) fn(fcall[(size_t)c2 * kFcCap + 2 + j]);
+      for (uint32_t j = lane; j + (kSpec - 2) < cnt; j += 32u) fn(sh_fckey[sh_fcoff[c2] + j]);
     };
     uint32_t need = k - G1;
     Key T = (Key)B1 << FS;
@@ -857,7 +947,7 @@ __global__ void __launch_bounds__(kCompressThreads, 1) compress_kernel(const Com
             const uint32_t i = j0 + lane;
             Key kk = T;
             if (i < cnt && !kDirectT)
-              kk = i < kSpec - 2 ? stage[c2 * kSpec + 2 + i] : fcall[(size_t)c2 * kFcCap + 2 + i];
+              kk = i < kSpec - 2 ? stage[c2 * kSpec + 2 + i] : sh_fckey[sh_fcoff[c2] + i - (kSpec - 2)];
             const bool valid = i < cnt;
             const uint32_t v = valid ? ((kk > T ? 0x10000u : 0u) | (kk == T ? 1u : 0u)) : 0u;
             const uint32_t incl = warp_incl_scan(v);
@@ -884,19 +974,40 @@ __global__ void __launch_bounds__(kCompressThreads, 1) compress_kernel(const Com
     };
     uint32_t o = sh_res[24] + kept_eq0 + w_aoff[w] + fcsel(w_boff[w]);
     uint32_t jfc = w_boff[w];
-    list_scan<Tr>(list, L, [&](bool valid, uint32_t idx, Bits b) {
-      const Key kk = Tr::key(b);
-      const uint32_t fb = (uint32_t)(kk >> FS);
-      const bool isfc = valid && fb == B1;
-      const uint32_t fm = __ballot_sync(kFull, isfc);
-      const uint32_t p = jfc + __popc(fm & lanemask_lt());
-      const bool keep_fc = kk > T || (kk == T && eq_before + (sh_fcpre[p] & 0xFFFFu) < need_eq);
-      const bool sel = valid && (fb > B1 || (isfc && keep_fc));
-      const uint32_t sm = __ballot_sync(kFull, sel);
-      if (sel) write_out<Tr>(a, o + __popc(sm & lanemask_lt()), idx, b);
-      o += __popc(sm);
-      jfc += __popc(fm);
-    });
+    const uint32_t lt = lanemask_lt();
+    auto walk = [&](auto frame_out) {
+      list_scan2<Tr>(list, L, [&](bool v0, uint32_t i0, Bits b0, bool v1, uint32_t i1, Bits b1) {
+        const Key k0 = Tr::key(b0), k1 = Tr::key(b1);
+        const uint32_t f0 = (uint32_t)(k0 >> FS), f1 = (uint32_t)(k1 >> FS);
+        const bool fc0 = v0 && f0 == B1, fc1 = v1 && f1 == B1;
+        const uint32_t m0 = __ballot_sync(kFull, fc0), m1 = __ballot_sync(kFull, fc1);
+        bool s0 = v0 && f0 > B1, s1 = v1 && f1 > B1;
+        if (m0 | m1) {  // final candidates: T and the tie quota decide
+          const uint32_t p0 = jfc + __popc(m0 & lt) + __popc(m1 & lt);
+          if (fc0) s0 = k0 > T || (k0 == T && eq_before + (sh_fcpre[p0] & 0xFFFFu) < need_eq);
+          if (fc1) s1 = k1 > T || (k1 == T && eq_before + (sh_fcpre[p0 + fc0] & 0xFFFFu) < need_eq);
+          jfc += __popc(m0) + __popc(m1);
+        }
+        const uint32_t q0 = __ballot_sync(kFull, s0), q1 = __ballot_sync(kFull, s1);
+        const uint32_t p = o + __popc(q0 & lt) + __popc(q1 & lt);
+        if constexpr (decltype(frame_out)::value) {  // reference frame: i64 indices, f32 values
+          if (s0) {
+            reinterpret_cast<int64_t*>(a.idx_out)[p] = (int64_t)i0;
+            reinterpret_cast<float*>(a.val_out)[p] = Tr::to_f32(b0);
+          }
+          if (s1) {
+            reinterpret_cast<int64_t*>(a.idx_out)[p + s0] = (int64_t)i1;
+            reinterpret_cast<float*>(a.val_out)[p + s0] = Tr::to_f32(b1);
+          }
+        } else {
+          if (s0) write_out<Tr>(a, p, i0, b0);
+          if (s1) write_out<Tr>(a, p + s0, i1, b1);
+        }
+        o += __popc(q0) + __popc(q1);
+      });
+    };
+    if (a.idx64 && a.val_f32 && a.val2_out == nullptr) walk(std::true_type{});
+    else walk(std::false_type{});
   } else {
     // ================= slow path: many keys share the fine bin B1 =================
     uint32_t need = k - G1;
@@ -993,10 +1104,15 @@ __global__ void __launch_bounds__(kCompressThreads, 1) compress_kernel(const Com
   STAMP(8);
   EXIT_AT(8);
 
-  // ---- leave the workspace clean: every bin this CTA added to its histogram
-  // replica lies in [my_lobin, my_maxb); all histogram / control reads
-  // happened before the last grid barrier.
-  for (uint32_t i = my_lobin + tid; i < my_maxb; i += kCompressThreads) hist[i] = 0u;
+  // ---- leave the workspace clean: the populated range of every replica,
+  // [pop_lo, pop_hi), is zeroed in 1/G slices (one CTA per slice, not one per
+  // contributor); all histogram / control reads happened before the last grid
+  // barrier.
+  {
+    const uint32_t span = pop_hi > pop_lo ? pop_hi - pop_lo : 0u;
+    for (uint32_t i = c * kCompressThreads + tid; i < span * kHistCopies; i += G * kCompressThreads)
+      a.hist1[(size_t)(i / span) * kFineBinsMax + pop_lo + i % span] = 0u;
+  }
   if (c == 0 && tid == 0) {
     ctrl[kCtrlMaxBin] = 0u;
     ctrl[kCtrlMaxLoBin] = 0u;

@@ -28,8 +28,14 @@
 namespace gp {
 
 constexpr int kDecThreads = 512;
-constexpr int kDecBlocksPerSm = 4;
-constexpr int kTileBytes = 16 * 1024;   // smem output tile (double-buffered)
+#ifndef GP_DEC_BLOCKS
+#define GP_DEC_BLOCKS 4
+#endif
+#ifndef GP_DEC_TILE_KB
+#define GP_DEC_TILE_KB 16
+#endif
+constexpr int kDecBlocksPerSm = GP_DEC_BLOCKS;
+constexpr int kTileBytes = GP_DEC_TILE_KB * 1024;   // smem output tile (double-buffered)
 constexpr int64_t kMinChunk = 8192;
 #ifndef GP_SPARSE_DENSITY_INV
 #define GP_SPARSE_DENSITY_INV 20
@@ -110,6 +116,32 @@ __device__ __forceinline__ int64_t warp_lower_bound(const IT* __restrict__ idx, 
   return lo + __popc(__ballot_sync(kFull, pred));
 }
 
+// The rest of a CTA's share of the adjacent-pair checks (idx[j] < idx[j+1]
+// for j in [j0, pe), stride kDecThreads), four independent load pairs in
+// flight per thread: at r = 10 a share is ~17 pairs per thread and a plain loop
+// is a serial chain of round trips at the end of the kernel.
+template <class IT>
+__device__ __forceinline__ bool pair_check_rest(const IT* __restrict__ idx, int64_t j0, int64_t pe) {
+  constexpr int U = 4;
+  bool bad = false;
+  for (int64_t j = j0; j < pe; j += U * kDecThreads) {
+    IT a[U], b[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t jj = j + (int64_t)u * kDecThreads;
+      a[u] = 0;
+      b[u] = 1;
+      if (jj < pe) {
+        a[u] = __ldg(idx + jj);
+        b[u] = __ldg(idx + jj + 1);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) bad |= !((int64_t)a[u] < (int64_t)b[u]);
+  }
+  return bad;
+}
+
 template <class IT, class VT, class OT>
 __global__ void __launch_bounds__(kDecThreads, kDecBlocksPerSm) decompress_kernel(
     const IT* __restrict__ idx, const VT* __restrict__ vals, int64_t k, int64_t d, int64_t chunk,
@@ -154,6 +186,10 @@ __global__ void __launch_bounds__(kDecThreads, kDecBlocksPerSm) decompress_kerne
   // (a block count) with no separate search round trip.
   int64_t ci = 0, ni = 0;
   VT cv = VT(0), nv = VT(0);
+#ifdef GP_DEC_DEEP
+  int64_t mi = 0;
+  VT mv = VT(0);
+#endif
   auto fetch = [&](int64_t b, int64_t& i, VT& v) {
     const int64_t j = b + tid;
     if (j >= 0 && j < k) {
@@ -197,6 +233,9 @@ __global__ void __launch_bounds__(kDecThreads, kDecBlocksPerSm) decompress_kerne
   }
   const bool have = fetch(base, ci, cv);
   bool nhave = fetch(base + kDecThreads, ni, nv);
+#ifdef GP_DEC_DEEP
+  bool mhave = fetch(base + 2 * kDecThreads, mi, mv);
+#endif
   bool pend = have && ci >= o0;  // entries below o0 belong to earlier CTAs
   DSTAMP(1);
   const bool vec_ok = ((uintptr_t)out % 16) == 0;
@@ -236,7 +275,14 @@ __global__ void __launch_bounds__(kDecThreads, kDecBlocksPerSm) decompress_kerne
       ci = ni;
       cv = nv;
       pend = nhave;
+#ifdef GP_DEC_DEEP
+      ni = mi;
+      nv = mv;
+      nhave = mhave;
+      mhave = fetch(base + 2 * kDecThreads, mi, mv);
+#else
       nhave = fetch(base + kDecThreads, ni, nv);
+#endif
     }
     if (full) {
       uint4* ov = reinterpret_cast<uint4*>(out + t0);
@@ -246,8 +292,7 @@ __global__ void __launch_bounds__(kDecThreads, kDecBlocksPerSm) decompress_kerne
     }
   }
   DSTAMP(3);
-  for (int64_t j = pb + tid + kDecThreads; j < pe; j += kDecThreads)
-    if (!((int64_t)__ldg(idx + j) < (int64_t)__ldg(idx + j + 1))) bad = true;
+  if (pair_check_rest(idx, pb + tid + kDecThreads, pe)) bad = true;
   if (__syncthreads_or(bad) && tid == 0) atomicOr(err, 2u);
   DSTAMP(4);
 #undef DSTAMP
@@ -327,8 +372,7 @@ __global__ void __launch_bounds__(kDecThreads, kDecBlocksPerSm) decompress_spars
     }
     if (__syncthreads_or(past)) break;
   }
-  for (int64_t j = pb + tid + kDecThreads; j < pe; j += kDecThreads)
-    if (!((int64_t)__ldg(idx + j) < (int64_t)__ldg(idx + j + 1))) bad = true;
+  if (pair_check_rest(idx, pb + tid + kDecThreads, pe)) bad = true;
   if (__syncthreads_or(bad) && tid == 0) atomicOr(err, 2u);
 }
 

@@ -19,7 +19,10 @@ constexpr int kLowBins = 256;           // smem low window (zeros, NaN, denormal
 constexpr int kFcCap = 8192;            // final-candidate capacity of the fast path
 
 // control words at the head of the workspace
-constexpr int kHistCopies = 8;          // replicas of the fine histogram (CTA c uses c % 8)
+#ifndef GP_HIST_COPIES
+#define GP_HIST_COPIES 2
+#endif
+constexpr int kHistCopies = GP_HIST_COPIES;  // replicas of the fine histogram (CTA c uses c % copies)
 constexpr int kCtrlBar = 0;             // grid-barrier word (top bit flips per barrier)
 constexpr int kCtrlMaxBin = 2;          // 1 + highest fine bin with a candidate
 constexpr int kCtrlMaxLoBin = 3;        // 1 + highest per-CTA watermark bin
