@@ -194,10 +194,27 @@ def run_ours(args, rank, world, local_rank):
                                       wsb, torch.cuda.current_stream(dev).cuda_stream)
         assert st == 0, st
 
-    def decompress(u, frame):
-        st = L.gp_topk_decompress_frame(frame.data_ptr(), u["k"], u["d"], u["out"].data_ptr(), 0, 0,
+    def decompress(u, frame_ptr):
+        st = L.gp_topk_decompress_frame(frame_ptr, u["k"], u["d"], u["out"].data_ptr(), 0, 0,
                                         err.data_ptr(), torch.cuda.current_stream(dev).cuda_stream)
         assert st == 0, st
+
+    # N>1 transport: "peer" = frames copied by the copy engines into the
+    # successor's receive buffer (CUDA IPC over NVLink, overlapping the next
+    # compress) and signalled with interprocess events; "nccl" = one
+    # batch_isend_irecv of all frames after the compress phase.
+    peer = world > 1 and args.transport == "peer"
+    ring = copy_stream = cpu_group = None
+    if peer:
+        from paper_2410_12707_b200.peer import PeerRing
+
+        cpu_group = dist.new_group(backend="gloo")
+        off = 0
+        for u in units:
+            u["off"] = off
+            off += (16 + 12 * u["k"] + 255) // 256 * 256
+        ring = PeerRing(off, dev, cpu_group)
+        copy_stream = torch.cuda.Stream(dev)
 
     def exchange():
         nxt, prv = (rank + 1) % world, (rank - 1) % world
@@ -208,63 +225,100 @@ def run_ours(args, rank, world, local_rank):
         for w in dist.batch_isend_irecv(ops):
             w.wait()
 
-    def compress_all(ev=None):
+    def compress_all(ev=None, parity=0):
+        cur = torch.cuda.current_stream(dev)
         for i, u in enumerate(units):
             if ev is not None:
-                ev[i][0].record(stream)
+                ev[i][0].record(cur)
             compress(u)
             if ev is not None:
-                ev[i][1].record(stream)
+                ev[i][1].record(cur)
+            if peer:  # frame i travels while frame i+1 is being compressed
+                done = torch.cuda.Event()
+                done.record(cur)
+                copy_stream.wait_event(done)
+                ring.copy(ring.peer_recv(parity) + u["off"], u["frame"].data_ptr(), 16 + 12 * u["k"], copy_stream)
+        if peer:
+            cur.wait_stream(copy_stream)
 
-    def decompress_all(ev=None):
+    def decompress_all(ev=None, parity=0):
+        cur = torch.cuda.current_stream(dev)
         for i, u in enumerate(units):
             if ev is not None:
-                ev[i][2].record(stream)
-            decompress(u, u["rframe"] if world > 1 else u["frame"])
+                ev[i][2].record(cur)
+            if peer:
+                src = ring.recv(parity) + u["off"]
+            else:
+                src = (u["rframe"] if world > 1 else u["frame"]).data_ptr()
+            decompress(u, src)
             if ev is not None:
-                ev[i][3].record(stream)
+                ev[i][3].record(cur)
+
+    def handoff():
+        """Between the compress and decompress phases of a step (N>1)."""
+        if peer:
+            ring.signal_sent(stream)
+            dist.barrier(group=cpu_group)  # every rank has recorded its 'sent' event (CPU only)
+            ring.wait_sent(stream)
+        else:
+            exchange()
+
+    parity = [0]
 
     def step(ev=None):
-        compress_all(ev)
+        p = parity[0]
+        parity[0] ^= 1
+        if peer:
+            ring.wait_consumed(stream)
+        compress_all(ev, p)
         if world > 1:
-            exchange()
-        decompress_all(ev)
+            handoff()
+        decompress_all(ev, p)
+        if peer:
+            ring.signal_consumed(stream)
 
     # The timed step replays two CUDA graphs (all compress launches, then all
     # decompress launches; the NCCL frame exchange runs eagerly in between at
     # N>1): launch-bound sequences of 24 kernels are what graphs are for.
     graphs = None
     if not args.no_graph:
+        step()  # first launches (kernel attributes are set outside any capture)
+        torch.cuda.synchronize(dev)
+        if world > 1:
+            dist.barrier()
         side = torch.cuda.Stream(dev)
         side.wait_stream(stream)
-        with torch.cuda.stream(side):
-            step()  # warm the launch path on the capture stream
-        stream.wait_stream(side)
-        torch.cuda.synchronize(dev)
-        graphs = []
-        for fn in (compress_all, decompress_all):
-            gph = torch.cuda.CUDAGraph()
-            with torch.cuda.graph(gph, stream=side):
-                fn()
-            graphs.append(gph)
+        graphs = {}
+        for par in ((0, 1) if peer else (0,)):
+            for name, fn in (("c", compress_all), ("d", decompress_all)):
+                gph = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(gph, stream=side):
+                    fn(None, par)
+                graphs[name, par] = gph
         torch.cuda.synchronize(dev)
 
     def timed_step(mid=None):
         """One step; `mid` = (event after the compress launches, event before the decompress launches)."""
+        p = parity[0] if peer else 0
+        parity[0] ^= 1
+        if peer:
+            ring.wait_consumed(stream)
         if graphs is None:
-            compress_all()
+            compress_all(None, p)
         else:
-            graphs[0].replay()
+            graphs["c", p].replay()
         if mid is not None:
             mid[0].record(stream)
         if world > 1:
-            exchange()
+            handoff()
         if mid is not None:
             mid[1].record(stream)
         if graphs is None:
-            decompress_all()
+            decompress_all(None, p)
         else:
-            graphs[1].replay()
+            graphs["d", p].replay()
+        if peer:
+            ring.signal_consumed(stream)
 
     def barrier():
         if world > 1:
@@ -362,7 +416,10 @@ def run_ours(args, rank, world, local_rank):
                               "2 CUDA graph replays per step (24 compress, then 24 decompress launches)"),
                    "kernel_times": "per-launch CUDA events from separate eager steps (roofline, per_config)",
                    "parallelism": ("replicas, no exchange" if world == 1 else
-                                   f"{world} ranks, compressed frames ring-exchanged over NCCL P2P (batch_isend_irecv)")},
+                                   f"{world} ranks, compressed frames ring-exchanged "
+                                   + ("by copy engines into the successor's buffer over NVLink (CUDA IPC, "
+                                      "overlapping the next compress; interprocess-event handoff)" if peer else
+                                      "over NCCL P2P (batch_isend_irecv)"))},
         "roofline": {"bound": "hbm", "kernel": "compress_kernel<f32> (cooperative, 1 CTA/SM)",
                      "achieved": round(achieved, 1), "peak": peak, "peak_kind": peak_kind, "unit": "GB/s",
                      "frac": round(achieved / peak, 4), "traffic": traffic,
@@ -408,21 +465,27 @@ def bench_e2e_dist(P, dev, rank, world, steps=2):
         for kind in KINDS:
             base = torch.randn(shape, generator=g)
             hosts.append((torch.relu(base) if kind == "activation" else base * 1e-3).reshape(-1).contiguous().pin_memory())
-    outs = [torch.empty_like(h).pin_memory() for h in hosts]
-    bufs = [torch.empty(h.numel(), device=dev) for h in hosts]
+    outs = [[torch.empty_like(h).pin_memory() for h in hosts] for _ in RATIOS]
+    bufs = [[torch.empty(h.numel(), device=dev) for h in hosts] for _ in RATIOS]
     nxt, prv = (rank + 1) % world, (rank - 1) % world
     total_bytes = sum(pair_bytes(h.numel(), 4, select_k(h.numel(), r)) for h in hosts for r in RATIOS)
     h2d = d2h = sum(h.numel() * 4 for h in hosts) * len(RATIOS)
+    main = torch.cuda.current_stream(dev)
+    copy = torch.cuda.Stream(dev)  # D2H reads of one ratio overlap the next ratio's H2D + codec + exchange
     times = []
     for s in range(steps + 1):
         dist.barrier()
         torch.cuda.synchronize(dev)
         t0 = time.perf_counter()
-        for r in RATIOS:
+        for ri, r in enumerate(RATIOS):
             xs = [h.to(dev, non_blocking=True) for h in hosts]
-            link.exchange([(x, r, nxt) for x in xs], [(b, r, prv) for b in bufs])
-            for b, o in zip(bufs, outs):
-                o.copy_(b)
+            link.exchange([(x, r, nxt) for x in xs], [(b, r, prv) for b in bufs[ri]])
+            done = torch.cuda.Event()
+            done.record(main)
+            copy.wait_event(done)
+            with torch.cuda.stream(copy):
+                for b, o in zip(bufs[ri], outs[ri]):
+                    o.copy_(b, non_blocking=True)
         torch.cuda.synchronize(dev)
         dt = time.perf_counter() - t0
         tt = torch.tensor([dt], device=dev)
@@ -528,6 +591,9 @@ def main():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--no-graph", action="store_true", help="timed steps as eager launches (no CUDA graphs)")
+    ap.add_argument("--transport", default="peer", choices=["peer", "nccl"],
+                    help="N>1 frame exchange: copy engines into the successor's buffer over NVLink (CUDA IPC), "
+                         "or NCCL batch_isend_irecv")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-pipeline", action="store_true", help="skip the GPT-2 pipeline sub-measurement")
     args = ap.parse_args()

@@ -118,6 +118,31 @@ int gp_adatopk_plan(const double* R, int n, double base_ratio,
 int gp_adatopk_plan_host(const double* R, int n, double base_ratio,
                          const int64_t* d_per_link, double* r_out, int64_t* k_out);
 
+/* ---- Stage-boundary transport over peer memory (NVLink / NVSwitch).
+ * Replaces the reference's in-process inbox delivery of compressed payloads
+ * (executor.py:248-297, `dest.inbox[key] = _maybe_decompress(...)`): a sender
+ * GPU copies its frames straight into the receiving GPU's buffer with the copy
+ * engines (no SMs, so transfers overlap the next compress) and signals an
+ * interprocess event the receiver's stream waits on.  Buffers and events are
+ * shared between processes as opaque 64-byte IPC handles. */
+#define GP_IPC_HANDLE_BYTES 64
+
+/* Device buffer that can be exported with gp_ipc_mem_handle. */
+int gp_peer_alloc(size_t bytes, void** ptr_out);
+int gp_peer_free(void* ptr);
+/* Export / import a gp_peer_alloc buffer (peer access enabled lazily). */
+int gp_ipc_mem_handle(void* ptr, void* handle_out);
+int gp_ipc_open_mem(const void* handle, void** ptr_out);
+int gp_ipc_close_mem(void* ptr);
+/* Interprocess event (timing disabled) and its import. */
+int gp_ipc_event_create(void** event_out, void* handle_out);
+int gp_ipc_open_event(const void* handle, void** event_out);
+int gp_event_destroy(void* event);
+int gp_event_record(void* event, void* stream);
+int gp_stream_wait_event(void* stream, void* event);
+/* Device-to-device (local or peer) async copy on `stream`. */
+int gp_copy_async(void* dst, const void* src, size_t bytes, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

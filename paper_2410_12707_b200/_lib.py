@@ -39,7 +39,20 @@ _SIGS = {
                                 POINTER(c_int64), POINTER(c_int32), c_void_p]),
     "gp_adatopk_plan_host": (c_int, [POINTER(c_double), c_int, c_double, POINTER(c_int64), POINTER(c_double),
                                      POINTER(c_int64)]),
+    # peer-memory transport (include/adatopk.h)
+    "gp_peer_alloc": (c_int, [c_size_t, POINTER(c_void_p)]),
+    "gp_peer_free": (c_int, [c_void_p]),
+    "gp_ipc_mem_handle": (c_int, [c_void_p, c_void_p]),
+    "gp_ipc_open_mem": (c_int, [c_void_p, POINTER(c_void_p)]),
+    "gp_ipc_close_mem": (c_int, [c_void_p]),
+    "gp_ipc_event_create": (c_int, [POINTER(c_void_p), c_void_p]),
+    "gp_ipc_open_event": (c_int, [c_void_p, POINTER(c_void_p)]),
+    "gp_event_destroy": (c_int, [c_void_p]),
+    "gp_event_record": (c_int, [c_void_p, c_void_p]),
+    "gp_stream_wait_event": (c_int, [c_void_p, c_void_p]),
+    "gp_copy_async": (c_int, [c_void_p, c_void_p, c_size_t, c_void_p]),
 }
+IPC_HANDLE_BYTES = 64
 
 EXPORTED = tuple(_SIGS)
 

@@ -10,6 +10,7 @@
 //   SparsePayload.to_bytes :39-44 -> the *_frame variants write/read that layout
 #include <cmath>
 #include <cstdio>
+#include <cstring>
 
 #include "../../include/adatopk.h"
 #include "gp_kernels.cuh"
@@ -217,6 +218,55 @@ int gp_adatopk_plan_host(const double* R, int n, double base_ratio, const int64_
                          int64_t* k_out) {
   if ((!R && n > 0) || n < 0) return GP_ERR_INVALID_ARGUMENT;
   return plan_impl(R, n, base_ratio, d_per_link, r_out, k_out);
+}
+
+// ---- peer-memory transport (executor.py:248-297 inbox delivery, on NVLink)
+static_assert(sizeof(cudaIpcMemHandle_t) == GP_IPC_HANDLE_BYTES, "IPC handle size");
+static_assert(sizeof(cudaIpcEventHandle_t) == GP_IPC_HANDLE_BYTES, "IPC event handle size");
+static int cuda_status(cudaError_t e) { return e == cudaSuccess ? GP_OK : GP_ERR_CUDA; }
+
+int gp_peer_alloc(size_t bytes, void** ptr_out) {
+  if (!ptr_out || bytes == 0) return GP_ERR_INVALID_ARGUMENT;
+  return cuda_status(cudaMalloc(ptr_out, bytes));
+}
+int gp_peer_free(void* ptr) { return cuda_status(cudaFree(ptr)); }
+int gp_ipc_mem_handle(void* ptr, void* handle_out) {
+  if (!ptr || !handle_out) return GP_ERR_INVALID_ARGUMENT;
+  return cuda_status(cudaIpcGetMemHandle(static_cast<cudaIpcMemHandle_t*>(handle_out), ptr));
+}
+int gp_ipc_open_mem(const void* handle, void** ptr_out) {
+  if (!handle || !ptr_out) return GP_ERR_INVALID_ARGUMENT;
+  cudaIpcMemHandle_t h;
+  std::memcpy(&h, handle, sizeof(h));
+  return cuda_status(cudaIpcOpenMemHandle(ptr_out, h, cudaIpcMemLazyEnablePeerAccess));
+}
+int gp_ipc_close_mem(void* ptr) { return cuda_status(cudaIpcCloseMemHandle(ptr)); }
+int gp_ipc_event_create(void** event_out, void* handle_out) {
+  if (!event_out || !handle_out) return GP_ERR_INVALID_ARGUMENT;
+  cudaEvent_t ev;
+  if (cudaEventCreateWithFlags(&ev, cudaEventDisableTiming | cudaEventInterprocess) != cudaSuccess) return GP_ERR_CUDA;
+  *event_out = ev;
+  return cuda_status(cudaIpcGetEventHandle(static_cast<cudaIpcEventHandle_t*>(handle_out), ev));
+}
+int gp_ipc_open_event(const void* handle, void** event_out) {
+  if (!handle || !event_out) return GP_ERR_INVALID_ARGUMENT;
+  cudaIpcEventHandle_t h;
+  std::memcpy(&h, handle, sizeof(h));
+  cudaEvent_t ev;
+  if (cudaIpcOpenEventHandle(&ev, h) != cudaSuccess) return GP_ERR_CUDA;
+  *event_out = ev;
+  return GP_OK;
+}
+int gp_event_destroy(void* event) { return cuda_status(cudaEventDestroy(static_cast<cudaEvent_t>(event))); }
+int gp_event_record(void* event, void* stream) {
+  return cuda_status(cudaEventRecord(static_cast<cudaEvent_t>(event), as_stream(stream)));
+}
+int gp_stream_wait_event(void* stream, void* event) {
+  return cuda_status(cudaStreamWaitEvent(as_stream(stream), static_cast<cudaEvent_t>(event), 0));
+}
+int gp_copy_async(void* dst, const void* src, size_t bytes, void* stream) {
+  if ((!dst || !src) && bytes) return GP_ERR_INVALID_ARGUMENT;
+  return cuda_status(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToDevice, as_stream(stream)));
 }
 
 }  // extern "C"

@@ -796,6 +796,11 @@ __global__ void __launch_bounds__(kCompressThreads, 1) compress_kernel(const Com
       fcreg[0] = (Key)sh_res[8];
       fcreg[1] = (Key)sh_res[9];
     }
+    if (tid < 256) {
+      sh_lvl[tid] = 0u;  // radix digit histograms of stage 3 (two levels, alternating)
+      sh_low[tid] = 0u;
+    }
+    if (tid < 2) sh_res[24 + tid] = 0u;
     STAMP(5);
     EXIT_AT(5);
     grid_barrier(bar, G);  // ---- B2
@@ -811,11 +816,11 @@ __global__ void __launch_bounds__(kCompressThreads, 1) compress_kernel(const Com
     Key* stage = reinterpret_cast<Key*>(smem + SL::coarse);  // coarse + window smem, free after stage 1
     static_assert(kMaxGridSpec * kSpec * sizeof(Key) <= (kCoarseBins + kWinBins) * 4, "staging fits");
     const Key* fcall = reinterpret_cast<const Key*>(a.fcreg);
-    if (tid < 256) {
-      sh_lvl[tid] = 0u;  // radix digit histograms (two levels, alternating)
-      sh_low[tid] = 0u;
-    }
-    if (tid < 2) sh_res[24 + tid] = 0u;
+    // the first radix level needs no prefix test (every FC key is in bin B1):
+    // its digit histogram is built straight from the gathered registers
+    const int nb0 = FS < 8 ? FS : 8;
+    const int lob0 = FS - nb0;
+    bool extra = false;  // some CTA holds more than kSpec-2 FC keys
     {
       Key v[R];
 #pragma unroll
@@ -826,14 +831,20 @@ __global__ void __launch_bounds__(kCompressThreads, 1) compress_kernel(const Com
 #pragma unroll
       for (int r = 0; r < R; ++r) {
         const uint32_t c2 = w + 32u * r;
-        if (c2 < G) stage[c2 * kSpec + lane] = v[r];
+        if (c2 < G) {
+          stage[c2 * kSpec + lane] = v[r];
+          const uint32_t cnt = (uint32_t)__shfl_sync(kFull, v[r], 1);
+          if (!kDirectT && lane >= 2 && lane - 2 < cnt)
+            atomicAdd(&sh_lvl[(uint32_t)(v[r] >> lob0) & ((1u << nb0) - 1u)], 1u);
+          extra |= cnt > kSpec - 2;
+        }
       }
     }
-    __syncthreads();
+    extra = __syncthreads_or(extra);
     // Keys beyond the first kSpec-2 of a CTA (many FC keys, e.g. r = 10 on a
     // large tensor) are fetched once, in one round trip, into sh_fckey
     // (flattened; sh_fcoff[c2] = offset of CTA c2's extras, sh_fcoff[G] = total).
-    if (!kDirectT) {
+    if (!kDirectT && extra) {
       if (w == 0) {
         const uint32_t per = (G + 31) / 32;
         uint32_t sx = 0;
@@ -873,7 +884,10 @@ __global__ void __launch_bounds__(kCompressThreads, 1) compress_kernel(const Com
 #pragma unroll
         for (int i = 0; i < PER; ++i) {
           const uint32_t p = tid + i * kCompressThreads;
-          if (p < nx) sh_fckey[p] = v[i];
+          if (p < nx) {
+            sh_fckey[p] = v[i];
+            atomicAdd(&sh_lvl[(uint32_t)(v[i] >> lob0) & ((1u << nb0) - 1u)], 1u);
+          }
         }
         __syncthreads();
       }
@@ -895,14 +909,16 @@ __global__ void __launch_bounds__(kCompressThreads, 1) compress_kernel(const Com
         const int nb = hib < 8 ? hib : 8;
         const int lob = hib - nb;
         uint32_t* H = (li & 1) ? sh_low : sh_lvl;
-        for (int r = 0; r < R; ++r) {
-          const uint32_t c2 = w + 32u * r;
-          if (c2 < G)
-            for_fc_keys(c2, [&](Key kk) {
-              if ((kk >> hib) == (T >> hib)) atomicAdd(&H[(uint32_t)(kk >> lob) & ((1u << nb) - 1u)], 1u);
-            });
+        if (li > 0) {  // level 0 was counted during the gather
+          for (int r = 0; r < R; ++r) {
+            const uint32_t c2 = w + 32u * r;
+            if (c2 < G)
+              for_fc_keys(c2, [&](Key kk) {
+                if ((kk >> hib) == (T >> hib)) atomicAdd(&H[(uint32_t)(kk >> lob) & ((1u << nb) - 1u)], 1u);
+              });
+          }
+          __syncthreads();
         }
-        __syncthreads();
         if (w == 0) {
           uint32_t dig = 0, above = 0;
           warp_cross_desc(H, (1 << nb) - 1, need, &dig, &above);
