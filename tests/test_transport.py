@@ -118,3 +118,77 @@ def test_ring_exchange_nccl_world2(cuda):
         pytest.skip("needs 2 GPUs (run under gpurun --gpus 2)")
     res = _run(2, "nccl")
     assert res == {0: True, 1: True}, res
+
+
+def _peer_worker(rank, world, port, q):
+    """Frames through PeerRing (copy engines into the successor's IPC buffer, event handoff)."""
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    try:
+        import ctypes
+
+        import paper_2410_12707_b200 as P
+        from paper_2410_12707_b200 import _lib
+        from paper_2410_12707_b200.peer import PeerRing
+
+        torch.cuda.set_device(rank)
+        dev = torch.device("cuda", rank)
+        dist.init_process_group("nccl", rank=rank, world_size=world, device_id=dev)
+        cpu = dist.new_group(backend="gloo")
+        L = _lib.lib()
+        d, r = 300_007, 50.0
+        k = P.select_k(d, r)
+        fb = 16 + 12 * k
+        ring = PeerRing(fb, dev, cpu)
+        st = torch.cuda.current_stream(dev)
+        cs = torch.cuda.Stream(dev)
+        out = torch.empty(d, device=dev)
+        err = torch.zeros(1, dtype=torch.int32, device=dev)
+        ok = True
+        for rnd in range(4):  # both buffer parities, twice
+            g = torch.Generator().manual_seed(1000 * rnd + rank)
+            x = torch.randn(d, generator=g).to(dev)
+            frame = torch.empty(fb, dtype=torch.uint8, device=dev)
+            wsb = L.gp_topk_workspace_bytes(d, 0)
+            ws = torch.zeros(wsb, dtype=torch.uint8, device=dev)
+            assert L.gp_topk_compress_frame(x.data_ptr(), 0, d, k, frame.data_ptr(), ws.data_ptr(), wsb,
+                                            st.cuda_stream) == 0
+            ring.wait_consumed(cs)
+            done = torch.cuda.Event()
+            done.record(st)
+            cs.wait_event(done)
+            ring.copy(ring.peer_recv(rnd), frame.data_ptr(), fb, cs)
+            st.wait_stream(cs)
+            ring.signal_sent(st)
+            dist.barrier(group=cpu)
+            ring.wait_sent(st)
+            assert L.gp_topk_decompress_frame(ring.recv(rnd), k, d, out.data_ptr(), 0, 0, err.data_ptr(),
+                                              st.cuda_stream) == 0
+            ring.signal_consumed(st)
+            torch.cuda.synchronize(dev)
+            prv = (rank - 1) % world
+            src = torch.randn(d, generator=torch.Generator().manual_seed(1000 * rnd + prv)).numpy()
+            vals, idx, _ = O.topk_compress(src, r)
+            ok &= int(err.item()) == 0
+            ok &= np.array_equal(out.cpu().numpy().view(np.uint32), O.topk_decompress(vals, idx, d).view(np.uint32))
+        dist.barrier()
+        ring.close()
+        dist.destroy_process_group()
+        q.put((rank, bool(ok)))
+    except Exception as e:
+        q.put((rank, repr(e)))
+
+
+@pytest.mark.gpu
+def test_peer_ring_world2(cuda):
+    if torch.cuda.device_count() < 2:
+        pytest.skip("needs 2 GPUs (run under gpurun --gpus 2)")
+    ctx = tmp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    ps = [ctx.Process(target=_peer_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in ps:
+        p.start()
+    res = dict(q.get(timeout=300) for _ in range(2))
+    for p in ps:
+        p.join(timeout=60)
+    assert res == {0: True, 1: True}, res
