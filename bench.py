@@ -181,17 +181,33 @@ def run_ours(args, rank, world, local_rank):
                               "out": torch.empty(d, device=dev)})
     dmax = max(u["d"] for u in units)
     wsb = L.gp_topk_workspace_bytes(dmax, 0)
-    ws = torch.empty(wsb, dtype=torch.uint8, device=dev)
+    # The 24 units are independent: they run on `streams` concurrent CUDA
+    # streams, each compress a cooperative grid of num_sms/streams CTAs with its
+    # own workspace, so one unit's barrier-bound tail overlaps the others' HBM
+    # streams.  Units go to streams longest-first (greedy on an HBM-bytes
+    # estimate), so the per-stream loads balance.
+    nstreams = max(1, args.streams)
+    num_sms = torch.cuda.get_device_properties(dev).multi_processor_count
+    ctas = 0 if nstreams == 1 else max(1, num_sms // nstreams)
+    wss = [torch.empty(wsb, dtype=torch.uint8, device=dev) for _ in range(nstreams)]
+    ws = wss[0]
+    load = [0.0] * nstreams
+    for u in sorted(units, key=lambda u: -(u["d"] * (1.6 if u["r"] <= 10 else 1.0))):
+        j = min(range(nstreams), key=lambda j: load[j])
+        u["sj"] = j
+        load[j] += u["d"] * (1.6 if u["r"] <= 10 else 1.0) + 2e6
     err = torch.zeros(1, dtype=torch.int32, device=dev)
     stream = torch.cuda.current_stream(dev)
     sp = stream.cuda_stream
-    assert L.gp_workspace_init(ws.data_ptr(), wsb, sp) == 0
+    for w_ in wss:
+        assert L.gp_workspace_init(w_.data_ptr(), wsb, sp) == 0
     flush = torch.ones(128 << 20, dtype=torch.float32, device=dev)  # 512 MB read between steps
     step_bytes = sum(pair_bytes(u["d"], 4, u["k"]) for u in units)
 
     def compress(u):  # on the current stream (the capture stream while a graph is recorded)
-        st = L.gp_topk_compress_frame(u["x"].data_ptr(), 0, u["d"], u["k"], u["frame"].data_ptr(), ws.data_ptr(),
-                                      wsb, torch.cuda.current_stream(dev).cuda_stream)
+        st = L.gp_topk_compress_frame_ctas(u["x"].data_ptr(), 0, u["d"], u["k"], u["frame"].data_ptr(),
+                                           wss[u["sj"]].data_ptr(), wsb, torch.cuda.current_stream(dev).cuda_stream,
+                                           ctas)
         assert st == 0, st
 
     def decompress(u, frame_ptr):
@@ -225,34 +241,49 @@ def run_ours(args, rank, world, local_rank):
         for w in dist.batch_isend_irecv(ops):
             w.wait()
 
-    def compress_all(ev=None, parity=0):
+    extra_streams = [torch.cuda.Stream(dev) for _ in range(nstreams - 1)]
+
+    def on_streams(body):
+        """Run body(i, u, st) for every unit on its stream: fork from, and join back into, the current stream."""
         cur = torch.cuda.current_stream(dev)
+        sts = [cur] + extra_streams
+        for s_ in extra_streams:
+            s_.wait_stream(cur)
         for i, u in enumerate(units):
+            st = sts[u["sj"]]
+            with torch.cuda.stream(st):
+                body(i, u, st)
+        for s_ in extra_streams:
+            cur.wait_stream(s_)
+
+    def compress_all(ev=None, parity=0):
+        def body(i, u, st):
             if ev is not None:
-                ev[i][0].record(cur)
+                ev[i][0].record(st)
             compress(u)
             if ev is not None:
-                ev[i][1].record(cur)
-            if peer:  # frame i travels while frame i+1 is being compressed
+                ev[i][1].record(st)
+            if peer:  # frame i travels while the next frames are being compressed
                 done = torch.cuda.Event()
-                done.record(cur)
+                done.record(st)
                 copy_stream.wait_event(done)
                 ring.copy(ring.peer_recv(parity) + u["off"], u["frame"].data_ptr(), 16 + 12 * u["k"], copy_stream)
+        on_streams(body)
         if peer:
-            cur.wait_stream(copy_stream)
+            torch.cuda.current_stream(dev).wait_stream(copy_stream)
 
     def decompress_all(ev=None, parity=0):
-        cur = torch.cuda.current_stream(dev)
-        for i, u in enumerate(units):
+        def body(i, u, st):
             if ev is not None:
-                ev[i][2].record(cur)
+                ev[i][2].record(st)
             if peer:
                 src = ring.recv(parity) + u["off"]
             else:
                 src = (u["rframe"] if world > 1 else u["frame"]).data_ptr()
             decompress(u, src)
             if ev is not None:
-                ev[i][3].record(cur)
+                ev[i][3].record(st)
+        on_streams(body)
 
     def handoff():
         """Between the compress and decompress phases of a step (N>1)."""
@@ -414,6 +445,8 @@ def run_ours(args, rank, world, local_rank):
                    "l2": "512 MB read flush between timed steps; each step reads 771 MB of inputs (> L2)",
                    "launch": ("eager launches" if args.no_graph else
                               "2 CUDA graph replays per step (24 compress, then 24 decompress launches)"),
+                   "concurrency": (f"units on {nstreams} concurrent streams, compress grids of {ctas or num_sms} "
+                                   f"CTAs, one workspace per stream"),
                    "kernel_times": "per-launch CUDA events from separate eager steps (roofline, per_config)",
                    "parallelism": ("replicas, no exchange" if world == 1 else
                                    f"{world} ranks, compressed frames ring-exchanged "
@@ -440,7 +473,7 @@ def run_ours(args, rank, world, local_rank):
         line["e2e"] = bench_e2e_dist(P, dev, rank, world)
     # the GPT-2 pipeline half of the BASELINE metric: GPT-2 medium, one stage
     # per GPU, AdaTopK r=100 on every FP/BP boundary (configs[2]; N=1 = no boundary)
-    del units, ws, flush
+    del units, ws, wss, flush
     torch.cuda.empty_cache()
     if not args.no_pipeline:
         from paper_2410_12707_b200 import pipeline as PL
@@ -591,6 +624,8 @@ def main():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--no-graph", action="store_true", help="timed steps as eager launches (no CUDA graphs)")
+    ap.add_argument("--streams", type=int, default=4,
+                    help="concurrent streams for the independent units (compress grid = num_sms / streams)")
     ap.add_argument("--transport", default="peer", choices=["peer", "nccl"],
                     help="N>1 frame exchange: copy engines into the successor's buffer over NVLink (CUDA IPC), "
                          "or NCCL batch_isend_irecv")

@@ -92,6 +92,14 @@ int gp_topk_decompress(const void* idx, int idx_bytes,
                        void* out, int out_dtype, int mode,
                        uint32_t* d_err_flag, void* stream);
 
+/* Same, with the cooperative grid capped at `max_ctas` CTAs (0 = one per SM):
+ * independent compresses on different streams (each with its own workspace)
+ * then share the GPU, one's barrier-bound tail overlapping another's HBM
+ * stream. */
+int gp_topk_compress_frame_ctas(const void* x, int dtype, int64_t d, int64_t k,
+                                void* frame_out, void* ws, size_t ws_bytes,
+                                void* stream, int max_ctas);
+
 /* Decompress straight from a reference wire frame on the device. */
 int gp_topk_decompress_frame(const void* frame, int64_t k, int64_t d,
                              void* out, int out_dtype, int mode,

@@ -127,8 +127,9 @@ int gp_workspace_init(void* ws, size_t ws_bytes, void* stream) {
   return cudaMemsetAsync(ws, 0, n, as_stream(stream)) == cudaSuccess ? GP_OK : GP_ERR_CUDA;
 }
 
-int gp_topk_compress(const void* x, int dtype, int64_t d, int64_t k, void* idx_out, int idx_bytes, void* val_out,
-                     int val_dtype, void* val2_out, void* header_out, void* ws, size_t ws_bytes, void* stream) {
+static int compress_impl(const void* x, int dtype, int64_t d, int64_t k, void* idx_out, int idx_bytes,
+                         void* val_out, int val_dtype, void* val2_out, void* header_out, void* ws, size_t ws_bytes,
+                         void* stream, int max_ctas) {
   if (d <= 0) return GP_ERR_EMPTY_VECTOR;
   if (!x || !idx_out || !val_out || !ws) return GP_ERR_INVALID_ARGUMENT;
   if (dtype < 0 || dtype > 2) return GP_ERR_INVALID_ARGUMENT;
@@ -140,6 +141,7 @@ int gp_topk_compress(const void* x, int dtype, int64_t d, int64_t k, void* idx_o
   if (ws_bytes < need) return GP_ERR_INVALID_ARGUMENT;
   gp::DeviceInfo dev;
   if (device_info(&dev)) return GP_ERR_CUDA;
+  dev.max_ctas = max_ctas;
   unsigned char* base = static_cast<unsigned char*>(ws);
   gp::CompressArgs a = {};
   a.x = x;
@@ -163,12 +165,23 @@ int gp_topk_compress(const void* x, int dtype, int64_t d, int64_t k, void* idx_o
   return gp::launch_compress(dtype, a, dev, as_stream(stream));
 }
 
+int gp_topk_compress(const void* x, int dtype, int64_t d, int64_t k, void* idx_out, int idx_bytes, void* val_out,
+                     int val_dtype, void* val2_out, void* header_out, void* ws, size_t ws_bytes, void* stream) {
+  return compress_impl(x, dtype, d, k, idx_out, idx_bytes, val_out, val_dtype, val2_out, header_out, ws, ws_bytes,
+                       stream, 0);
+}
+
+int gp_topk_compress_frame_ctas(const void* x, int dtype, int64_t d, int64_t k, void* frame_out, void* ws,
+                                size_t ws_bytes, void* stream, int max_ctas) {
+  if (!frame_out || ((uintptr_t)frame_out % 8) != 0 || max_ctas < 0) return GP_ERR_INVALID_ARGUMENT;
+  unsigned char* f = static_cast<unsigned char*>(frame_out);
+  return compress_impl(x, dtype, d, k, f + GP_FRAME_HEADER_BYTES, 8, f + GP_FRAME_HEADER_BYTES + 8 * k,
+                       GP_DTYPE_F32, nullptr, f, ws, ws_bytes, stream, max_ctas);
+}
+
 int gp_topk_compress_frame(const void* x, int dtype, int64_t d, int64_t k, void* frame_out, void* ws,
                            size_t ws_bytes, void* stream) {
-  if (!frame_out || ((uintptr_t)frame_out % 8) != 0) return GP_ERR_INVALID_ARGUMENT;
-  unsigned char* f = static_cast<unsigned char*>(frame_out);
-  return gp_topk_compress(x, dtype, d, k, f + GP_FRAME_HEADER_BYTES, 8, f + GP_FRAME_HEADER_BYTES + 8 * k,
-                          GP_DTYPE_F32, nullptr, f, ws, ws_bytes, stream);
+  return gp_topk_compress_frame_ctas(x, dtype, d, k, frame_out, ws, ws_bytes, stream, 0);
 }
 
 static int decompress_common(const void* idx, int idx_bytes, const void* vals, int val_dtype, int64_t k, int64_t d,

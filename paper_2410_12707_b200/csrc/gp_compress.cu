@@ -1181,7 +1181,8 @@ static int launch_compress_t(CompressArgs a, const DeviceInfo& dev, cudaStream_t
     max_blocks_per_sm[dev.ordinal] = nb;
     configured[dev.ordinal] = 1;
   }
-  const uint32_t gmax = (uint32_t)std::min(dev.num_sms * max_blocks_per_sm[dev.ordinal], kMaxGridSpec);
+  uint32_t gmax = (uint32_t)std::min(dev.num_sms * max_blocks_per_sm[dev.ordinal], kMaxGridSpec);
+  if (dev.max_ctas > 0) gmax = std::min(gmax, (uint32_t)dev.max_ctas);
   const uint32_t G =
       (uint32_t)std::min<uint64_t>(gmax, std::max<uint64_t>(1, ((uint64_t)a.d + kMinPerCta - 1) / kMinPerCta));
   const uint64_t per_unit = ((uint64_t)a.d + (uint64_t)G * 32 - 1) / ((uint64_t)G * 32);

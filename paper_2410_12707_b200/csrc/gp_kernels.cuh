@@ -59,6 +59,7 @@ struct WsLayout {
 struct DeviceInfo {
   int ordinal;
   int num_sms;
+  int max_ctas = 0;  // compress grid cap (0: one CTA per SM); lets independent compresses share the GPU
 };
 
 int launch_compress(int dtype, CompressArgs a, const DeviceInfo& dev, cudaStream_t stream);
