@@ -422,3 +422,35 @@ def test_decompress_frame_large_k_both_kernels(cuda, ratio):
     ref = torch.zeros_like(x)
     ref[idx] = x[idx]
     assert torch.equal(out, ref)
+
+
+@pytest.mark.parametrize("ratio", [10, 1000])
+def test_capped_grid_and_concurrent_streams_identical_frames(cuda, ratio):
+    """gp_topk_compress_frame_ctas: any grid cap (1 CTA .. one per SM) gives the
+    byte-identical reference frame, also with four compresses in flight on
+    four streams (one workspace each), as the benchmark runs them."""
+    L = _lib.lib()
+    g = torch.Generator(device=cuda).manual_seed(ratio)
+    xs = [torch.relu(torch.randn(2_000_003, device=cuda, generator=g)) if i % 2 else
+          torch.randn(2_000_003, device=cuda, generator=g) * 1e-3 for i in range(4)]
+    d = xs[0].numel()
+    k = P.select_k(d, ratio)
+    wsb = L.gp_topk_workspace_bytes(d, _lib.DTYPE_F32)
+    wss = [torch.zeros(wsb, dtype=torch.uint8, device=cuda) for _ in range(4)]
+    expect = [O.compress_frame(x.cpu().numpy(), ratio, "threshold") for x in xs]
+    s = torch.cuda.current_stream().cuda_stream
+    for ctas in (1, 7, 37, 74, 0):
+        f = torch.empty(16 + 12 * k, dtype=torch.uint8, device=cuda)
+        assert L.gp_topk_compress_frame_ctas(xs[0].data_ptr(), 0, d, k, f.data_ptr(), wss[0].data_ptr(), wsb, s,
+                                             ctas) == 0
+        assert f.cpu().numpy().tobytes() == expect[0], ctas
+    streams = [torch.cuda.Stream(cuda) for _ in range(4)]
+    frames = [torch.empty(16 + 12 * k, dtype=torch.uint8, device=cuda) for _ in range(4)]
+    torch.cuda.synchronize()
+    for rep in range(3):
+        for i, st in enumerate(streams):
+            assert L.gp_topk_compress_frame_ctas(xs[i].data_ptr(), 0, d, k, frames[i].data_ptr(), wss[i].data_ptr(),
+                                                 wsb, st.cuda_stream, 37) == 0
+        torch.cuda.synchronize()
+        for i in range(4):
+            assert frames[i].cpu().numpy().tobytes() == expect[i], (rep, i)
