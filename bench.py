@@ -220,7 +220,7 @@ def run_ours(args, rank, world, local_rank):
     # compress) and signalled with interprocess events; "nccl" = one
     # batch_isend_irecv of all frames after the compress phase.
     peer = world > 1 and args.transport == "peer"
-    ring = copy_stream = cpu_group = None
+    ring = copy_streams = cpu_group = None
     if peer:
         from paper_2410_12707_b200.peer import PeerRing
 
@@ -230,7 +230,7 @@ def run_ours(args, rank, world, local_rank):
             u["off"] = off
             off += (16 + 12 * u["k"] + 255) // 256 * 256
         ring = PeerRing(off, dev, cpu_group)
-        copy_stream = torch.cuda.Stream(dev)
+        copy_streams = [torch.cuda.Stream(dev) for _ in range(max(1, args.streams))]  # one per compute stream
 
     def exchange():
         nxt, prv = (rank + 1) % world, (rank - 1) % world
@@ -264,13 +264,15 @@ def run_ours(args, rank, world, local_rank):
             if ev is not None:
                 ev[i][1].record(st)
             if peer:  # frame i travels while the next frames are being compressed
+                cs = copy_streams[u["sj"]]
                 done = torch.cuda.Event()
                 done.record(st)
-                copy_stream.wait_event(done)
-                ring.copy(ring.peer_recv(parity) + u["off"], u["frame"].data_ptr(), 16 + 12 * u["k"], copy_stream)
+                cs.wait_event(done)
+                ring.copy(ring.peer_recv(parity) + u["off"], u["frame"].data_ptr(), 16 + 12 * u["k"], cs)
         on_streams(body)
         if peer:
-            torch.cuda.current_stream(dev).wait_stream(copy_stream)
+            for cs in copy_streams:
+                torch.cuda.current_stream(dev).wait_stream(cs)
 
     def decompress_all(ev=None, parity=0):
         def body(i, u, st):
