@@ -173,6 +173,8 @@ def run_ours(args, rank, world, local_rank):
             x = torch.relu(base) if kind == "activation" else base * 1e-3
             x = x.reshape(-1).contiguous()
             for r in RATIOS:
+                if os.environ.get("GP_BENCH_ONLY_R") and float(os.environ["GP_BENCH_ONLY_R"]) != r:
+                    continue  # development aid: a subset of the workload
                 d = x.numel()
                 k = select_k(d, r)
                 units.append({"x": x, "d": d, "k": k, "r": r, "shape": shape, "kind": kind,

@@ -294,12 +294,6 @@ __device__ __forceinline__ unsigned long long globaltimer_ns() {
     }                                                                   \
   } while (0)
 
-// per-warp cycle stamps (lane 0): a.dbg[32768 + unit * 16 + slot]
-#define WSTAMP(slot)                                                                         \
-  do {                                                                                       \
-    if (a.dbg != nullptr && lane == 0) a.dbg[32768 + (size_t)unit * 16 + (slot)] = clock64(); \
-  } while (0)
-
 // ---------------------------------------------------------------------------
 // shared-memory layout (bytes)
 
@@ -370,56 +364,48 @@ __global__ void __launch_bounds__(kCompressThreads, 1) compress_kernel(const Com
   uint32_t* bar = &ctrl[kCtrlBar];
   // this CTA's histogram replica (kHistCopies replicas cut same-address atomic contention)
   uint32_t* hist = a.hist1 + (size_t)(c & (kHistCopies - 1)) * kFineBinsMax;
-  WSTAMP(0);
 
   STAMP(0);
-  if (GP_EXIT_AT == 10) return;
   if (a.header != nullptr && c == 0 && tid == 0) {
     a.header[0] = (unsigned long long)d;
     a.header[1] = (unsigned long long)k;
   }
 
-  // ---- the unit's rows (1 KiB each) stream through a per-warp ring of
-  // kRing shared-memory slots, filled by bulk (TMA) copies on one mbarrier per
-  // slot; the first kRing rows are requested before anything else
+  // ---- the unit's rows (1 KiB each) stream through a per-warp ring of two
+  // 2 KiB slots, each holding a row pair filled by one bulk (TMA) copy that
+  // completes on the slot's mbarrier; the first two pairs are requested before
+  // anything else
   const uint32_t nch = a.aligned ? n / EPL : 0u;  // full 32-byte chunks in the unit
   const uint32_t nrow = (nch + 31) / 32;
+  const uint32_t npair = (nrow + 1) / 2;
   const uint32_t* xw = reinterpret_cast<const uint32_t*>(x + u0);
+  constexpr uint32_t kPairs = kRing / 2;            // row-pair slots per warp
   const uint32_t ring = smem_addr(smem + SL::ring) + w * (kRing * 1024u);
   const uint32_t mbar = smem_addr(smem + SL::mbar) + w * (kRing * 8u);
   const uint64_t policy = l2_evict_first_policy();  // x is read once: keep L2 for the lists
-  uint32_t seq = 0;                                 // rows this warp has issued into the ring
-  auto issue = [&](uint32_t r, uint32_t q) {        // lane 0: row r as ring sequence number q
-    const uint32_t slot = q % kRing;
-    bulk_load_async(ring + slot * 1024u, xw + (size_t)r * 256u, min(32u, nch - r * 32u) * 32u, mbar + slot * 8u,
+  uint32_t seq = 0;                                 // row pairs this warp has issued into the ring
+  auto issue = [&](uint32_t p, uint32_t q) {        // lane 0: row pair p as ring sequence number q
+    const uint32_t slot = q % kPairs;
+    bulk_load_async(ring + slot * 2048u, xw + (size_t)p * 512u, min(64u, nch - p * 64u) * 32u, mbar + slot * 8u,
                     policy);
   };
   if (lane == 0) {
-    for (uint32_t s = 0; s < kRing; ++s) mbar_init(mbar + s * 8u, 1u);
+    for (uint32_t s = 0; s < kPairs; ++s) mbar_init(mbar + s * 8u, 1u);
     fence_mbar_init();
-    for (uint32_t r = 0; r < min(nrow, kRing); ++r) issue(r, r);
+    for (uint32_t p = 0; p < min(npair, kPairs); ++p) issue(p, p);
     // a short unit sends its remaining rows to L2 now (no second HBM round trip)
     if (nrow > kRing && nrow <= kRing + kPrefetchRows)
       prefetch_l2_bulk(xw + (size_t)kRing * 256u, (nch - kRing * 32u) * 32u);
   }
   __syncwarp();
 
-  if (GP_EXIT_AT == 11 || GP_EXIT_AT == 12) {
-    if (GP_EXIT_AT == 12)
-      for (uint32_t r = 0; r < min(nrow, kRing); ++r) mbar_wait(mbar + r * 8u, 0u);
-    else if (lane == 0)
-      for (uint32_t r = 0; r < min(nrow, kRing); ++r) mbar_wait(mbar + r * 8u, 0u);
-    __syncwarp();
-    return;
-  }
   // ---- stage 0: low watermark from a sample of this CTA's row 0s (no extra
   // traffic): 4 elements per lane, one warp finds the crossing from the top
   for (uint32_t i = tid; i < kCoarseBins; i += kCompressThreads) sh_coarse[i] = 0u;
   if (tid < 32) sh_res[tid] = 0u;
   __syncthreads();
   if (nrow > 0) {
-    mbar_wait(mbar, 0u);
-    WSTAMP(1);
+    mbar_wait(mbar, 0u);  // row pair 0
     uint32_t ns = 0, mb = 0;
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
@@ -460,7 +446,10 @@ __global__ void __launch_bounds__(kCompressThreads, 1) compress_kernel(const Com
   const uint32_t top = min(nfine, ((cmax + 1u) << (FB - 12)) + (2u << (FB - Tr::kExpBits)));
 
   STAMP(1);
-  EXIT_AT(1);
+  if (GP_EXIT_AT == 1) {  // drain the ring first: no bulk copy may outlive the CTA
+    for (uint32_t p = 0; p < min(npair, kPairs); ++p) mbar_wait(mbar + p * 8u, 0u);
+    return;
+  }
   uint32_t L = 0;                              // this warp's candidate count
   uint32_t my_lobin = (uint32_t)(lo0 >> FS);   // lowest fine bin this CTA histograms
 
@@ -589,29 +578,23 @@ __global__ void __launch_bounds__(kCompressThreads, 1) compress_kernel(const Com
         count_new(from);
       }
     };
-    static_assert(kRing % 2 == 0, "rows are consumed in pairs");
+    static_assert(kRing == 4, "two row-pair slots");
     const uint32_t q0 = seq;
     if (!preloaded && lane == 0) {
       fence_proxy_async_smem();
-      for (uint32_t r = 0; r < min(nrow, kRing); ++r) issue(r, q0 + r);
+      for (uint32_t p = 0; p < min(npair, kPairs); ++p) issue(p, q0 + p);
     }
-    for (uint32_t r = 0; r < nrow; r += 2) {
-      const uint32_t q = q0 + r, s0 = q % kRing, s1 = (q + 1) % kRing;
-      mbar_wait(mbar + s0 * 8u, (q / kRing) & 1u);
-      if (r + 1 < nrow) mbar_wait(mbar + s1 * 8u, ((q + 1) / kRing) & 1u);
-      if (r < 12 && preloaded) WSTAMP(2 + r);
-#ifndef GP_EXP_NOPROCESS
-      process2(r, ring + s0 * 1024u, ring + s1 * 1024u);
-#endif
+    for (uint32_t p = 0; p < npair; ++p) {
+      const uint32_t q = q0 + p, slot = q % kPairs;
+      mbar_wait(mbar + slot * 8u, (q / kPairs) & 1u);
+      process2(2u * p, ring + slot * 2048u, ring + slot * 2048u + 1024u);
       __syncwarp();
-      if (lane == 0 && r + kRing < nrow) {  // refill the two slots just consumed
+      if (lane == 0 && p + kPairs < npair) {  // refill the slot just consumed
         fence_proxy_async_smem();
-        issue(r + kRing, q + kRing);
-        if (r + kRing + 1 < nrow) issue(r + kRing + 1, q + kRing + 1);
+        issue(p + kPairs, q + kPairs);
       }
     }
-    seq = q0 + nrow;
-    if (preloaded) WSTAMP(14);
+    seq = q0 + npair;
     const Key span = lo ? Tr::kInfAbs - lo_m1 : ~(Key)0;
     for (uint32_t i0 = nch * EPL; i0 < n; i0 += 32u) {  // scalar tail / unaligned input
       const uint32_t i = i0 + lane;
@@ -634,7 +617,6 @@ __global__ void __launch_bounds__(kCompressThreads, 1) compress_kernel(const Com
       if (L) atomicAdd(&sh_res[20], L);
     }
     __syncthreads();
-    if (preloaded) WSTAMP(15);
     for (uint32_t i = tid; i < kWinBins; i += kCompressThreads) {
       const uint32_t v = sh_win[i];
       if (v) red_add_gpu(&hist[wb + i], v);

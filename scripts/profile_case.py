@@ -20,6 +20,7 @@ def main():
     ap.add_argument("--ratio", type=float, default=100.0)
     ap.add_argument("--iters", type=int, default=5)
     ap.add_argument("--dtype", default="f32", choices=["f32", "bf16"])
+    ap.add_argument("--ctas", type=int, default=0, help="compress grid cap (0: one CTA per SM)")
     args = ap.parse_args()
     dev = torch.device("cuda", 0)
     shape = tuple(int(s) for s in args.shape.split(","))
@@ -42,7 +43,8 @@ def main():
     flush = torch.ones(128 << 20, dtype=torch.float32, device=dev)
     for _ in range(args.iters):
         flush.sum()
-        assert L.gp_topk_compress_frame(x.data_ptr(), code, d, k, frame.data_ptr(), ws.data_ptr(), wsb, st) == 0
+        assert L.gp_topk_compress_frame_ctas(x.data_ptr(), code, d, k, frame.data_ptr(), ws.data_ptr(), wsb, st,
+                                             args.ctas) == 0
         assert L.gp_topk_decompress_frame(frame.data_ptr(), k, d, out.data_ptr(), code, 0, err.data_ptr(), st) == 0
     torch.cuda.synchronize()
     assert int(err.item()) == 0
