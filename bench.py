@@ -194,10 +194,18 @@ def run_ours(args, rank, world, local_rank):
     wss = [torch.empty(wsb, dtype=torch.uint8, device=dev) for _ in range(nstreams)]
     ws = wss[0]
     load = [0.0] * nstreams
-    for u in sorted(units, key=lambda u: -(u["d"] * (1.6 if u["r"] <= 10 else 1.0))):
+    per_stream = [[] for _ in range(nstreams)]
+    for i in sorted(range(len(units)), key=lambda i: -(units[i]["d"] * (1.6 if units[i]["r"] <= 10 else 1.0))):
         j = min(range(nstreams), key=lambda j: load[j])
-        u["sj"] = j
-        load[j] += u["d"] * (1.6 if u["r"] <= 10 else 1.0) + 2e6
+        units[i]["sj"] = j
+        per_stream[j].append(i)
+        load[j] += units[i]["d"] * (1.6 if units[i]["r"] <= 10 else 1.0) + 2e6
+    # odd streams run their units smallest-first, so the barrier-bound tails of
+    # concurrent kernels do not line up
+    if os.environ.get("GP_BENCH_STAGGER", "1") == "1":
+        for j in range(1, nstreams, 2):
+            per_stream[j].reverse()
+    stream_order = [i for lst in per_stream for i in lst]
     err = torch.zeros(1, dtype=torch.int32, device=dev)
     stream = torch.cuda.current_stream(dev)
     sp = stream.cuda_stream
@@ -251,7 +259,8 @@ def run_ours(args, rank, world, local_rank):
         sts = [cur] + extra_streams
         for s_ in extra_streams:
             s_.wait_stream(cur)
-        for i, u in enumerate(units):
+        for i in stream_order:
+            u = units[i]
             st = sts[u["sj"]]
             with torch.cuda.stream(st):
                 body(i, u, st)

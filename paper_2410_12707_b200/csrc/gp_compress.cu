@@ -562,19 +562,27 @@ __global__ void __launch_bounds__(kCompressThreads, 1) compress_kernel(const Com
           }
           L += run;
         }
-        // append (divergent): each candidate is one LDS from its ring slot
+        // append (divergent): each candidate is one LDS from its ring slot;
+        // once a warp's list is past its smem part (dense steps), entries go
+        // straight to global memory without a per-entry placement test
+        auto append = [&](auto glob_only) {
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          uint32_t mm = m[j];
-          const uint32_t piece = (j & 1) * 32u + lane;
-          const uint32_t base = u0 + (r + (j >> 1)) * (32u * EPL) + piece * EPS;
-          const uint32_t src = (j < 2 ? so0 : so1) + piece * 16u;
-          while (mm) {
-            const uint32_t e = __ffs(mm) - 1;
-            mm &= mm - 1;
-            list.put(pos[j]++, base + e, ld_shared_elem<Tr>(src + e * (uint32_t)sizeof(Elem)));
+          for (int j = 0; j < 4; ++j) {
+            uint32_t mm = m[j];
+            const uint32_t piece = (j & 1) * 32u + lane;
+            const uint32_t base = u0 + (r + (j >> 1)) * (32u * EPL) + piece * EPS;
+            const uint32_t src = (j < 2 ? so0 : so1) + piece * 16u;
+            while (mm) {
+              const uint32_t e = __ffs(mm) - 1;
+              mm &= mm - 1;
+              const Bits bv = ld_shared_elem<Tr>(src + e * (uint32_t)sizeof(Elem));
+              if constexpr (decltype(glob_only)::value) Entry<Tr>::put(list.glob, pos[j]++, base + e, bv);
+              else list.put(pos[j]++, base + e, bv);
+            }
           }
-        }
+        };
+        if (from >= kCap) append(std::true_type{});
+        else append(std::false_type{});
         count_new(from);
       }
     };
