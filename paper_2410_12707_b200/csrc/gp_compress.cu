@@ -457,8 +457,11 @@ __global__ void __launch_bounds__(kCompressThreads, 1) compress_kernel(const Com
   // histogram those whose fine bin is below add_below
   auto stream_unit = [&](Key lo, uint32_t add_below, bool preloaded) {
     const uint32_t lob = (uint32_t)(lo >> FS);
-    uint32_t wb = top > (uint32_t)kWinBins ? top - kWinBins : 0u;
-    wb = max(wb, lob);
+    // smem window: candidates are densest right above the watermark, so the
+    // window starts there (at 20 fine bits it spans only two octaves); with no
+    // watermark (every element a candidate) it ends at the top of the sample
+    // range.  Bins outside it take global atomics.
+    uint32_t wb = lob > 0u ? lob : (top > (uint32_t)kWinBins ? top - kWinBins : 0u);
     wb = min(wb, nfine - kWinBins);
     const uint32_t lowlim = min((uint32_t)kLowBins, wb);
     for (uint32_t i = tid; i < kWinBins; i += kCompressThreads) sh_win[i] = 0u;
