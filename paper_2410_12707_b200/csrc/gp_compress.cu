@@ -718,7 +718,9 @@ __global__ void __launch_bounds__(kCompressThreads, 1) compress_kernel(const Com
   // (except bin 0, which holds both NaN, key 0, and +-0, key 1)
   const bool kDirectT = Tr::kDirectT && B1 != 0;
 
-  if (M + 2 <= (uint32_t)kFcCap) {
+  // fast path: the final candidates fit the per-CTA windows (bf16: they are
+  // all equal to T, so only their per-CTA counts are exchanged and any number fits)
+  if (kDirectT || M + 2 <= (uint32_t)kFcCap) {
     // ================= fast path =================
     // Each CTA's FC region: [0] sure count, [1] FC count, [2..] FC keys in
     // index order, so one coalesced read of 32 words per CTA after B2 returns
@@ -950,7 +952,7 @@ __global__ void __launch_bounds__(kCompressThreads, 1) compress_kernel(const Com
           }
           acc_a += (lane == 0 ? (uint32_t)stage[c2 * kSpec] : 0u) + gt;
           acc_e += eq;
-        } else {  // own CTA: sh_fcpre[i] = (gt << 16) | eq over own keys before i
+        } else if (!kDirectT) {  // own CTA: sh_fcpre[i] = (gt << 16) | eq over own keys before i
           uint32_t run = 0;
           for (uint32_t j0 = 0; j0 < cnt; j0 += 32u) {
             const uint32_t i = j0 + lane;
@@ -978,6 +980,7 @@ __global__ void __launch_bounds__(kCompressThreads, 1) compress_kernel(const Com
     const uint32_t kept_eq0 = min(eq_before, need_eq);
     // kept own final candidates before own FC position p
     auto fcsel = [&](uint32_t p) {
+      if (kDirectT) return min(eq_before + p, need_eq) - kept_eq0;  // every own FC key == T
       const uint32_t v = sh_fcpre[p];
       return (v >> 16) + min(eq_before + (v & 0xFFFFu), need_eq) - kept_eq0;
     };
@@ -993,8 +996,13 @@ __global__ void __launch_bounds__(kCompressThreads, 1) compress_kernel(const Com
         bool s0 = v0 && f0 > B1, s1 = v1 && f1 > B1;
         if (m0 | m1) {  // final candidates: T and the tie quota decide
           const uint32_t p0 = jfc + __popc(m0 & lt) + __popc(m1 & lt);
-          if (fc0) s0 = k0 > T || (k0 == T && eq_before + (sh_fcpre[p0] & 0xFFFFu) < need_eq);
-          if (fc1) s1 = k1 > T || (k1 == T && eq_before + (sh_fcpre[p0 + fc0] & 0xFFFFu) < need_eq);
+          if (kDirectT) {
+            if (fc0) s0 = eq_before + p0 < need_eq;
+            if (fc1) s1 = eq_before + p0 + fc0 < need_eq;
+          } else {
+            if (fc0) s0 = k0 > T || (k0 == T && eq_before + (sh_fcpre[p0] & 0xFFFFu) < need_eq);
+            if (fc1) s1 = k1 > T || (k1 == T && eq_before + (sh_fcpre[p0 + fc0] & 0xFFFFu) < need_eq);
+          }
           jfc += __popc(m0) + __popc(m1);
         }
         const uint32_t q0 = __ballot_sync(kFull, s0), q1 = __ballot_sync(kFull, s1);

@@ -244,6 +244,17 @@ def test_bf16_large_vs_oracle(cuda):
         assert dense.dtype == torch.bfloat16
 
 
+def test_bf16_heavy_ties_vs_oracle(cuda):
+    """bf16 at 16M elements, r=10 and 3: tens of thousands of keys equal the
+    threshold value (bf16 has 128 values per octave), far beyond the
+    final-candidate window capacity; ties must still go to the lower indices."""
+    g = torch.Generator(device=cuda).manual_seed(44)
+    x = torch.randn(16 * 1024 * 1024, device=cuda, generator=g).to(torch.bfloat16)
+    for r in (10, 3):
+        p = _check_against_oracle(x, r)
+        assert torch.equal(p.values, x.reshape(-1)[p.indices])
+
+
 def test_f64_vs_oracle(cuda):
     g = torch.Generator(device=cuda).manual_seed(5)
     x = torch.randn(300_001, device=cuda, generator=g, dtype=torch.float64)
