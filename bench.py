@@ -478,12 +478,86 @@ def run_ours(args, rank, world, local_rank):
         "gpu_launches": 2 * len(units) * args.steps,
         "clocks": clk,
     }
+    if world == 1 and not args.no_graph:
+        # int32-index wire (8 B per kept element instead
+        # of the reference's 12; Eq. 6's expansion factor becomes 2), same
+        # units, streams and timing as the timed steps
+        for u in units:
+            u["i32"] = torch.empty(u["k"], dtype=torch.int32, device=dev)
+            u["v32"] = torch.empty(u["k"], dtype=torch.float32, device=dev)
+
+        def c32_all(ev=None, par=0):
+            def body(i, u, st):
+                assert L.gp_topk_compress_ctas(u["x"].data_ptr(), 0, u["d"], u["k"], u["i32"].data_ptr(), 4,
+                                               u["v32"].data_ptr(), 0, None, None, wss[u["sj"]].data_ptr(), wsb,
+                                               st.cuda_stream, ctas) == 0
+            on_streams(body)
+
+        def d32_all(ev=None, par=0):
+            def body(i, u, st):
+                assert L.gp_topk_decompress(u["i32"].data_ptr(), 4, u["v32"].data_ptr(), 0, u["k"], u["d"],
+                                            u["out"].data_ptr(), 0, 0, err.data_ptr(), st.cuda_stream) == 0
+            on_streams(body)
+
+        g32 = []
+        for fn in (c32_all, d32_all):
+            fn()
+            torch.cuda.synchronize(dev)
+            gph = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(gph, stream=side):
+                fn()
+            g32.append(gph)
+        t32 = []
+        for _ in range(max(3, args.steps)):
+            flush.sum()
+            barrier()
+            s0, s1 = mk(), mk()
+            s0.record(stream)
+            g32[0].replay()
+            g32[1].replay()
+            s1.record(stream)
+            barrier()
+            t32.append(s0.elapsed_time(s1))
+        assert int(err.item()) == 0
+        b32 = sum(2 * (u["d"] * 4 + 8 * u["k"]) for u in units)
+        line["wire_int32"] = {"ms_per_step": round(statistics.mean(t32), 4),
+                              "value": round(b32 / (statistics.mean(t32) * 1e-3) / 1e9, 2), "unit": "GB/s",
+                              "frame_bytes_per_step": sum(8 * u["k"] for u in units),
+                              "reference_wire_frame_bytes_per_step": sum(16 + 12 * u["k"] for u in units),
+                              "note": "int32 indices + f32 values (8 B/elem), algorithmic bytes d*4 + 8k per launch"}
     if rank == 0 and world == 1:
         line["c1_gpt2_small"] = bench_c1(P, L, dev, flush, peak)
         line["cpu_baseline"] = cpu_baseline()
         line["e2e"] = bench_e2e(P, dev)
     elif world > 1:
         line["e2e"] = bench_e2e_dist(P, dev, rank, world)
+    if peer:
+        # transfers: one step's frames pushed into the
+        # successor's buffer by the copy engines, timed alone, every rank at once
+        tb = sum(16 + 12 * u["k"] for u in units)
+        barrier()
+        e0, e1 = mk(), mk()
+        e0.record(stream)
+        for cs in copy_streams:
+            cs.wait_stream(stream)
+        for u in units:  # over the copy streams, as in the timed steps
+            ring.copy(ring.peer_recv(0) + u["off"], u["frame"].data_ptr(), 16 + 12 * u["k"], copy_streams[u["sj"]])
+        for cs in copy_streams:
+            stream.wait_stream(cs)
+        e1.record(stream)
+        barrier()
+        t_copy = e0.elapsed_time(e1) * 1e-3
+        tt = torch.tensor([t_copy], device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        t_copy = float(tt.item())
+        line["transfer"] = {"payload_bytes_per_step_per_rank": tb, "peer_copy_gbs": round(tb / t_copy / 1e9, 1),
+                            "nvlink_peak_gbs_per_direction": 900.0,
+                            "frac_of_nvlink": round(tb / t_copy / 1e9 / 900.0, 3),
+                            "dense_equivalent_gbs": round(world * sum(4 * u["d"] for u in units) / (t_step * 1e-3)
+                                                          / 1e9, 1),
+                            "how": "all frames of one step copied to the successor by the copy engines (one copy "
+                                   "stream per compute stream), timed alone, max over ranks; in the timed steps these "
+                                   "copies overlap the compresses"}
     # the GPT-2 pipeline half of the BASELINE metric: GPT-2 medium, one stage
     # per GPU, AdaTopK r=100 on every FP/BP boundary (configs[2]; N=1 = no boundary)
     del units, ws, wss, flush

@@ -92,6 +92,13 @@ int gp_topk_decompress(const void* idx, int idx_bytes,
                        void* out, int out_dtype, int mode,
                        uint32_t* d_err_flag, void* stream);
 
+/* gp_topk_compress with the cooperative grid capped at `max_ctas` CTAs (see
+ * gp_topk_compress_frame_ctas). */
+int gp_topk_compress_ctas(const void* x, int dtype, int64_t d, int64_t k,
+                          void* idx_out, int idx_bytes, void* val_out, int val_dtype,
+                          void* val2_out, void* header_out, void* ws, size_t ws_bytes,
+                          void* stream, int max_ctas);
+
 /* Same, with the cooperative grid capped at `max_ctas` CTAs (0 = one per SM):
  * independent compresses on different streams (each with its own workspace)
  * then share the GPU, one's barrier-bound tail overlapping another's HBM

@@ -29,6 +29,8 @@ _SIGS = {
                                  c_void_p, c_void_p, c_void_p, c_size_t, c_void_p]),
     "gp_topk_compress_frame": (c_int, [c_void_p, c_int, c_int64, c_int64, c_void_p, c_void_p, c_size_t,
                                        c_void_p]),
+    "gp_topk_compress_ctas": (c_int, [c_void_p, c_int, c_int64, c_int64, c_void_p, c_int, c_void_p, c_int,
+                                      c_void_p, c_void_p, c_void_p, c_size_t, c_void_p, c_int]),
     "gp_topk_compress_frame_ctas": (c_int, [c_void_p, c_int, c_int64, c_int64, c_void_p, c_void_p, c_size_t,
                                             c_void_p, c_int]),
     "gp_topk_decompress": (c_int, [c_void_p, c_int, c_void_p, c_int, c_int64, c_int64, c_void_p, c_int, c_int,

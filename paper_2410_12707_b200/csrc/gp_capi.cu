@@ -171,6 +171,14 @@ int gp_topk_compress(const void* x, int dtype, int64_t d, int64_t k, void* idx_o
                        stream, 0);
 }
 
+int gp_topk_compress_ctas(const void* x, int dtype, int64_t d, int64_t k, void* idx_out, int idx_bytes, void* val_out,
+                          int val_dtype, void* val2_out, void* header_out, void* ws, size_t ws_bytes, void* stream,
+                          int max_ctas) {
+  if (max_ctas < 0) return GP_ERR_INVALID_ARGUMENT;
+  return compress_impl(x, dtype, d, k, idx_out, idx_bytes, val_out, val_dtype, val2_out, header_out, ws, ws_bytes,
+                       stream, max_ctas);
+}
+
 int gp_topk_compress_frame_ctas(const void* x, int dtype, int64_t d, int64_t k, void* frame_out, void* ws,
                                 size_t ws_bytes, void* stream, int max_ctas) {
   if (!frame_out || ((uintptr_t)frame_out % 8) != 0 || max_ctas < 0) return GP_ERR_INVALID_ARGUMENT;
