@@ -566,6 +566,9 @@ def run_ours(args, rank, world, local_rank):
         from paper_2410_12707_b200 import pipeline as PL
 
         line["pipeline"] = PL.run_pipeline("medium", "uniform", 100.0, n_micro=8, steps=3, warmup=2)
+        if world > 1:  # Eq. 6 on the device from measured link times
+            line["pipeline_measured_adatopk"] = PL.run_pipeline("medium", "measured", 100.0, n_micro=8, steps=3,
+                                                                warmup=1)
         if world == 8:  # configs[3]: GPT-2 XL, 8 stages, Eq. 6 ratios from a two-cluster link model
             line["pipeline_xl_adatopk"] = PL.run_pipeline("xl", "adatopk", 100.0, steps=2, warmup=1)
     return line

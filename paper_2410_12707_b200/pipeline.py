@@ -29,7 +29,7 @@ import torch.distributed as dist
 import torch.nn as nn
 import torch.nn.functional as F
 
-from .compressor import CompressionPlan, adatopk_plan, select_k, uniform_plan
+from .compressor import CompressionPlan, adatopk_plan, adatopk_plan_device, select_k, uniform_plan
 from .transport import FrameCodec, frame_bytes
 
 _P2P_BATCHED = os.environ.get("GP_P2P_BATCHED", "1") == "1"  # batched single-op P2P (0: plain isend/irecv)
@@ -152,6 +152,56 @@ def two_cluster_link_times(n_stages: int, boundary_bytes: int, fast=(1e-5, 1 / 1
     mid = n_stages // 2 - 1
     return [(slow if s == mid else fast)[0] + (slow if s == mid else fast)[1] * boundary_bytes
             for s in range(n_stages - 1)]
+
+
+def measure_link_times(shape, device, reps: int = 5) -> list:
+    """Measured dense boundary transfer time (s) of every FP link s -> s+1.
+
+    Each rank sends a dense boundary tensor to its successor while receiving
+    from its predecessor (one batched NCCL group, so the links run at once, as
+    in the pipeline); the receiver times its receive with CUDA events (median of
+    `reps`).  An all-reduce gives every rank the same vector, so every rank
+    derives the same per-link plan (both ends of a link agree on k).  This is
+    R_i of Eq. 6 measured instead of the alpha-beta estimate of the reference
+    CLI (cli.py:51-59).
+    """
+    rank, S = dist.get_rank(), dist.get_world_size()
+    x = torch.randn(shape, device=device)
+    buf = torch.empty(shape, device=device)
+    t = torch.zeros(max(S - 1, 1), dtype=torch.float64, device=device)
+    samples = []
+    for _ in range(reps + 1):
+        dist.barrier()
+        ops = []
+        if rank < S - 1:
+            ops.append(dist.P2POp(dist.isend, x, rank + 1))
+        if rank > 0:
+            ops.append(dist.P2POp(dist.irecv, buf, rank - 1))
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        for w in dist.batch_isend_irecv(ops):
+            w.wait()
+        b.record()
+        torch.cuda.synchronize()
+        samples.append(a.elapsed_time(b) * 1e-3)
+    if rank > 0:
+        samples = sorted(samples[1:])
+        t[rank - 1] = samples[len(samples) // 2]
+    dist.all_reduce(t)
+    return t.tolist()
+
+
+def measured_link_plan(n_stages: int, ratio: float, link_times: list, boundary: int, device) -> CompressionPlan:
+    """Eq. 6 on the device from measured link times (FP time mirrored onto BP)."""
+    links = [(s, s + 1) for s in range(n_stages - 1)] + [(s + 1, s) for s in range(n_stages - 1)]
+    R = torch.tensor(list(link_times) + list(link_times), dtype=torch.float64, device=device)
+    dl = torch.full((len(links),), boundary, dtype=torch.int64, device=device)
+    r, _k, status = adatopk_plan_device(R, ratio, dl)
+    st = int(status.item())
+    if st != 0:
+        from .errors import raise_for_status
+        raise_for_status(st, "gp_adatopk_plan")
+    return CompressionPlan(base_ratio=ratio, per_link={lk: float(v) for lk, v in zip(links, r.tolist())})
 
 
 @dataclass
@@ -300,8 +350,13 @@ def run_pipeline(model: str = "medium", plan_mode: str = "uniform", ratio: float
     n_micro = n_micro or max(4, 2 * world)
     dev = torch.device("cuda", torch.cuda.current_device())
     boundary = mb * seq_len * cfg.n_embd
-    lt = two_cluster_link_times(world, boundary * 4) if plan_mode == "adatopk" else None
-    plan = link_plan(world, plan_mode, ratio, lt)
+    lt = None
+    if plan_mode == "measured" and world > 1:
+        lt = measure_link_times((mb, seq_len, cfg.n_embd), dev)
+        plan = measured_link_plan(world, ratio, lt, boundary, dev)
+    else:
+        lt = two_cluster_link_times(world, boundary * 4) if plan_mode == "adatopk" else None
+        plan = link_plan(world, plan_mode, ratio, lt)
     pipe = DistPipeline(cfg, plan, mb, seq_len) if world > 1 else VirtualPipeline(cfg, 1, None, dev)
     gb = mb * n_micro
     times, loss = [], float("nan")
@@ -334,6 +389,9 @@ def run_pipeline(model: str = "medium", plan_mode: str = "uniform", ratio: float
             "n_micro": n_micro, "global_batch": gb, "seq_len": seq_len, "ms_per_step": round(t, 2),
             "loss": round(loss, 4), "plan": plan_mode if world > 1 else "none (1 stage, no boundary)",
             "base_ratio": ratio, "boundary_elems": boundary, "dense_boundary_bytes": boundary * 4, "links": links,
+            "link_times_s": [round(v, 7) for v in lt] if lt is not None else None,
+            "link_times_source": {"measured": "dense boundary P2P, CUDA events, median (measure_link_times)",
+                                  "adatopk": "two-cluster alpha-beta model"}.get(plan_mode),
             "schedule": "GPipe fill-drain (executor.py:389-404), bf16 autocast, fp32 boundaries",
             "partition": "contiguous equal layers (OP-Fence split of a homogeneous chain)",
             "data": "synthetic tokens, random init"}
@@ -346,5 +404,5 @@ def synthetic_batch(cfg: GPT2Config, batch: int, seq_len: int, device, seed: int
 
 
 __all__ = ["GPT2Config", "GPT2_SMALL", "GPT2_MEDIUM", "GPT2_XL", "GPT2_TINY", "partition", "make_stage",
-           "link_plan", "two_cluster_link_times", "VirtualPipeline", "DistPipeline", "synthetic_batch", "run_pipeline",
+           "link_plan", "two_cluster_link_times", "measure_link_times", "measured_link_plan", "VirtualPipeline", "DistPipeline", "synthetic_batch", "run_pipeline",
            ]

@@ -26,7 +26,7 @@ def main():
     ap.add_argument("--micro-batch", type=int, default=None)
     ap.add_argument("--n-micro", type=int, default=None)
     ap.add_argument("--seq", type=int, default=1024)
-    ap.add_argument("--plan", default="uniform", choices=["none", "uniform", "adatopk"])
+    ap.add_argument("--plan", default="uniform", choices=["none", "uniform", "adatopk", "measured"])
     ap.add_argument("--ratio", type=float, default=100.0)
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=2)

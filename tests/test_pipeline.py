@@ -134,3 +134,47 @@ def test_dist_pipeline_matches_virtual(cuda):
         ref.append(pipe.step(tok, tgt, n_micro=4))
     for a, b in zip(res[0], ref):
         assert abs(a - b) <= 1e-2 * abs(b), (res[0], ref)
+
+
+def _measured_worker(rank, world, port, q):
+    import torch.distributed as dist
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    try:
+        torch.cuda.set_device(rank)
+        dev = torch.device("cuda", rank)
+        dist.init_process_group("nccl", rank=rank, world_size=world, device_id=dev)
+        lt = PL.measure_link_times((2, 64, PL.GPT2_TINY.n_embd), dev, reps=3)
+        plan = PL.measured_link_plan(world, 10.0, lt, 2 * 64 * PL.GPT2_TINY.n_embd, dev)
+        pipe = PL.DistPipeline(PL.GPT2_TINY, plan, micro_batch=2, seq_len=64, lr=1e-3, seed=3)
+        tok, tgt = PL.synthetic_batch(PL.GPT2_TINY, 8, 64, dev, seed=0)
+        loss = pipe.step(tok, tgt, n_micro=4)
+        dist.barrier()
+        dist.destroy_process_group()
+        q.put((rank, (lt, sorted(plan.per_link.items()), loss)))
+    except Exception as e:
+        q.put((rank, repr(e)))
+
+
+@pytest.mark.gpu
+def test_measured_link_plan_agrees_on_both_ranks(cuda):
+    """Eq. 6 from measured link times, on the device; both ends of the link derive
+    the same ratio (hence k) and the slowest link gets 3r."""
+    if torch.cuda.device_count() < 2:
+        pytest.skip("needs 2 GPUs (run under gpurun --gpus 2)")
+    import torch.multiprocessing as tmp
+
+    ctx = tmp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    ps = [ctx.Process(target=_measured_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in ps:
+        p.start()
+    res = dict(q.get(timeout=600) for _ in range(2))
+    for p in ps:
+        p.join(timeout=60)
+    assert isinstance(res[0], tuple) and isinstance(res[1], tuple), res
+    assert res[0][0] == res[1][0] and res[0][1] == res[1][1]  # same link times, same plan
+    ratios = [r for _, r in res[0][1]]
+    assert max(ratios) == 30.0 and all(r >= 1.0 for r in ratios)
+    assert res[0][0][0] > 0 and np.isfinite(res[0][2])
