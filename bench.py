@@ -651,10 +651,61 @@ def bench_c1(P, L, dev, flush, peak, reps=20):
             td.append(e[1].elapsed_time(e[2]) * 1e3)
     c, dd = statistics.median(tc), statistics.median(td)
     b = pair_bytes(d, 4, k)
-    return {"shape": list(C1_SHAPE), "ratio": 100, "compress_us": round(c, 2), "decompress_us": round(dd, 2),
-            "pair_us": round(c + dd, 2), "pair_gbs": round(b / ((c + dd) * 1e-6) / 1e9, 1),
-            "frac_of_peak": round(b / ((c + dd) * 1e-6) / 1e9 / peak, 4),
-            "note": "per-launch CUDA events after a 512 MB L2 flush; includes launch latency"}
+    res = {"shape": list(C1_SHAPE), "ratio": 100, "compress_us": round(c, 2), "decompress_us": round(dd, 2),
+           "pair_us": round(c + dd, 2), "pair_gbs": round(b / ((c + dd) * 1e-6) / 1e9, 1),
+           "frac_of_peak": round(b / ((c + dd) * 1e-6) / 1e9 / peak, 4),
+           "note": "one tensor: per-launch CUDA events after a 512 MB L2 flush; includes launch latency"}
+    # Throughput on GPT-2 activation shapes: the n_micro = 8 boundary tensors of
+    # one pipeline flush, compress+decompress each, over 4 streams (37-CTA
+    # grids, a workspace per stream), one CUDA graph, L2 flushed before each rep
+    n, ns = 8, 4
+    ctas = max(1, torch.cuda.get_device_properties(dev).multi_processor_count // ns)
+    xs = [torch.randn(C1_SHAPE, device=dev, generator=g).reshape(-1) for _ in range(n)]
+    frames = [torch.empty(16 + 12 * k, dtype=torch.uint8, device=dev) for _ in range(n)]
+    outs = [torch.empty(d, device=dev) for _ in range(n)]
+    wss = [torch.empty(wsb, dtype=torch.uint8, device=dev) for _ in range(ns)]
+    for w_ in wss:
+        L.gp_workspace_init(w_.data_ptr(), wsb, sp)
+    main = torch.cuda.current_stream(dev)
+    sts = [torch.cuda.Stream(dev) for _ in range(ns)]
+
+    def batch():
+        cur = torch.cuda.current_stream(dev)
+        for st in sts:
+            st.wait_stream(cur)
+        for i in range(n):
+            st = sts[i % ns]
+            assert L.gp_topk_compress_frame_ctas(xs[i].data_ptr(), 0, d, k, frames[i].data_ptr(),
+                                                 wss[i % ns].data_ptr(), wsb, st.cuda_stream, ctas) == 0
+            assert L.gp_topk_decompress_frame(frames[i].data_ptr(), k, d, outs[i].data_ptr(), 0, 0, err.data_ptr(),
+                                              st.cuda_stream) == 0
+        for st in sts:
+            cur.wait_stream(st)
+
+    batch()
+    torch.cuda.synchronize(dev)
+    side = torch.cuda.Stream(dev)
+    side.wait_stream(main)
+    gph = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(gph, stream=side):
+        batch()
+    tb = []
+    for i in range(reps + 3):
+        flush.sum()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(main)
+        gph.replay()
+        e1.record(main)
+        e1.synchronize()
+        if i >= 3:
+            tb.append(e0.elapsed_time(e1) * 1e3)
+    assert int(err.item()) == 0
+    t = statistics.median(tb)
+    res["batch8_4streams"] = {"tensors": n, "us": round(t, 2), "gbs": round(n * b / (t * 1e-6) / 1e9, 1),
+                              "frac_of_peak": round(n * b / (t * 1e-6) / 1e9 / peak, 4),
+                              "note": "8 independent C1 tensors (one pipeline flush of boundaries), compress then "
+                                      "decompress each, 4 streams x 37-CTA grids, one CUDA graph"}
+    return res
 
 
 def cpu_baseline():
