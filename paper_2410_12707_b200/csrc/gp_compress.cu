@@ -512,12 +512,13 @@ __global__ void __launch_bounds__(kCompressThreads, 1) compress_kernel(const Com
     // i.e. elements [h*32*EPS + lane*EPS, +EPS).
     auto process2 = [&](uint32_t r, uint32_t so0, uint32_t so1) {
       uint32_t m[4];
+      const bool full = (r + 2u) * 32u <= nch;  // both rows complete: no per-piece bounds
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
         const uint32_t rr = r + (j >> 1);
         const uint32_t piece = (j & 1) * 32u + lane;
         uint32_t mm = 0;
-        if (rr < nrow && piece < 2u * min(32u, nch - rr * 32u)) {
+        if (full || (rr < nrow && piece < 2u * min(32u, nch - rr * 32u))) {
           const uint4 v = ld_shared_v4((j < 2 ? so0 : so1) + piece * 16u);
 #pragma unroll
           for (int e = 0; e < EPS; ++e)
@@ -525,8 +526,12 @@ __global__ void __launch_bounds__(kCompressThreads, 1) compress_kernel(const Com
         }
         m[j] = mm;
       }
-      const uint64_t packed = (uint64_t)__popc(m[0]) | ((uint64_t)__popc(m[1]) << 16) |
-                              ((uint64_t)__popc(m[2]) << 32) | ((uint64_t)__popc(m[3]) << 48);
+      // per-sub-row counts packed into one scan: 8-bit fields when a sub-row
+      // holds at most 32*EPS <= 128 candidates (f32, f64), else 16-bit fields
+      constexpr int kField = EPS * 32 < 256 ? 8 : 16;
+      using Packed = typename std::conditional<kField == 8, uint32_t, uint64_t>::type;
+      const Packed packed = (Packed)__popc(m[0]) | ((Packed)__popc(m[1]) << kField) |
+                            ((Packed)__popc(m[2]) << (2 * kField)) | ((Packed)__popc(m[3]) << (3 * kField));
       // sparse step (the common case above r ~ 50): no lane holds two
       // candidates in one sub-row, so ballots give every position directly and
       // each candidate is histogrammed where it is appended
@@ -548,20 +553,23 @@ __global__ void __launch_bounds__(kCompressThreads, 1) compress_kernel(const Com
         return;
       }
       if (__any_sync(kFull, packed != 0)) {
-        const uint64_t incl = warp_incl_scan64(packed);
-        const uint64_t excl = incl - packed, tot = __shfl_sync(kFull, incl, 31);
+        Packed incl;
+        if constexpr (kField == 8) incl = warp_incl_scan(packed);
+        else incl = warp_incl_scan64(packed);
+        const Packed excl = incl - packed, tot = __shfl_sync(kFull, incl, 31);
+        constexpr uint32_t kMask = (1u << kField) - 1u;
         const uint32_t from = L;
         uint32_t pos[4];
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
-          pos[j] = L + ((uint32_t)(excl >> (16 * j)) & 0xFFFFu);
+          pos[j] = L + ((uint32_t)(excl >> (kField * j)) & kMask);
         }
         {  // every earlier sub-row's total precedes sub-row j
           uint32_t run = 0;
 #pragma unroll
           for (int j = 0; j < 4; ++j) {
             pos[j] += run;
-            run += (uint32_t)(tot >> (16 * j)) & 0xFFFFu;
+            run += (uint32_t)(tot >> (kField * j)) & kMask;
           }
           L += run;
         }
