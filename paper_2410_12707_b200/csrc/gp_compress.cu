@@ -53,6 +53,7 @@ namespace gp {
 
 constexpr int kMaxGridSpec = 160;      // largest grid: the one-round-trip FC gather stages G*32 keys in smem
 constexpr uint32_t kRing = 4;          // 1 KiB rows in flight per warp (bulk copies into smem)
+constexpr uint32_t kFcCapBig = 65536;  // final candidates the fast path accepts in total
 #ifndef GP_PREFETCH_ROWS
 #define GP_PREFETCH_ROWS 8
 #endif
@@ -726,9 +727,12 @@ __global__ void __launch_bounds__(kCompressThreads, 1) compress_kernel(const Com
   // (except bin 0, which holds both NaN, key 0, and +-0, key 1)
   const bool kDirectT = Tr::kDirectT && B1 != 0;
 
-  // fast path: the final candidates fit the per-CTA windows (bf16: they are
-  // all equal to T, so only their per-CTA counts are exchanged and any number fits)
-  if (kDirectT || M + 2 <= (uint32_t)kFcCap) {
+  // fast path: every CTA's final candidates fit its window (bf16: they are
+  // all equal to T, so only their per-CTA counts are exchanged and any number
+  // fits).  Up to kFcCapBig in total they usually do; a CTA that overflows is
+  // seen by every CTA after B2 and all of them take the slow path.
+  bool fast = kDirectT || M + 2 <= kFcCapBig;
+  if (fast) {
     // ================= fast path =================
     // Each CTA's FC region: [0] sure count, [1] FC count, [2..] FC keys in
     // index order, so one coalesced read of 32 words per CTA after B2 returns
@@ -774,8 +778,9 @@ __global__ void __launch_bounds__(kCompressThreads, 1) compress_kernel(const Com
     if (!kDirectT) {  // publish the staged keys at the warp's place in the CTA's index order
       const uint32_t cb = w_b[w];
       Key* dst = fcreg + 2 + w_boff[w];
-      for (uint32_t i = lane; i < min(cb, kStageW); i += 32u) dst[i] = stagew[i];
-      if (cb > kStageW) {  // rare: this warp alone holds more than its staging share
+      const uint32_t room = sub_sat(kFcCap - 2, w_boff[w]);  // never past the CTA's region
+      for (uint32_t i = lane; i < min(min(cb, kStageW), room); i += 32u) dst[i] = stagew[i];
+      if (cb > kStageW && room > kStageW) {  // rare: this warp alone holds more than its staging share
         uint32_t r = 0;
         for (uint32_t base = 0; base < L; base += 32u) {
           const uint32_t j = base + lane;
@@ -790,7 +795,7 @@ __global__ void __launch_bounds__(kCompressThreads, 1) compress_kernel(const Com
           }
           const uint32_t fm = __ballot_sync(kFull, isfc);
           const uint32_t p = r + __popc(fm & lanemask_lt());
-          if (isfc && p >= kStageW) dst[p] = kk;
+          if (isfc && p >= kStageW && p < room) dst[p] = kk;
           r += __popc(fm);
         }
       }
@@ -847,15 +852,20 @@ __global__ void __launch_bounds__(kCompressThreads, 1) compress_kernel(const Com
     // Keys beyond the first kSpec-2 of a CTA (many FC keys, e.g. r = 10 on a
     // large tensor) are fetched once, in one round trip, into sh_fckey
     // (flattened; sh_fcoff[c2] = offset of CTA c2's extras, sh_fcoff[G] = total).
+    bool xg = false;  // the extras exceed smem: read them from the CTA regions
     if (!kDirectT && extra) {
       if (w == 0) {
         const uint32_t per = (G + 31) / 32;
-        uint32_t sx = 0;
+        uint32_t sx = 0, mx = 0;
         for (uint32_t i = 0; i < per; ++i) {
           const uint32_t c2 = lane * per + i;
-          if (c2 < G) sx += sub_sat((uint32_t)stage[c2 * kSpec + 1], kSpec - 2);
+          if (c2 < G) {
+            sx += sub_sat((uint32_t)stage[c2 * kSpec + 1], kSpec - 2);
+            mx = max(mx, (uint32_t)stage[c2 * kSpec + 1]);
+          }
         }
         const uint32_t incl = warp_incl_scan(sx);
+        mx = __reduce_max_sync(kFull, mx);
         uint32_t run = incl - sx;
         for (uint32_t i = 0; i < per; ++i) {
           const uint32_t c2 = lane * per + i;
@@ -864,11 +874,16 @@ __global__ void __launch_bounds__(kCompressThreads, 1) compress_kernel(const Com
             run += sub_sat((uint32_t)stage[c2 * kSpec + 1], kSpec - 2);
           }
         }
-        if (lane == 31) sh_fcoff[G] = incl;
+        if (lane == 31) {
+          sh_fcoff[G] = incl;
+          sh_res[26] = mx > (uint32_t)kFcCap - 2;  // some CTA's keys overflowed its region
+        }
       }
       __syncthreads();
       const uint32_t nx = sh_fcoff[G];
-      if (nx) {
+      if (sh_res[26]) {
+        fast = false;  // the same decision in every CTA
+      } else if (nx <= (uint32_t)kFcCap) {
         constexpr int PER = kFcCap / kCompressThreads;
         Key v[PER];
 #pragma unroll
@@ -893,14 +908,29 @@ __global__ void __launch_bounds__(kCompressThreads, 1) compress_kernel(const Com
           }
         }
         __syncthreads();
+      } else {  // very many final candidates (r ~ 10 on >= 2^26 elements): extras stay in global memory
+        xg = true;
+        for (uint32_t r = 0; r < (G + 31) / 32; ++r) {
+          const uint32_t c2 = w + 32u * r;
+          if (c2 < G) {
+            const uint32_t cnt = (uint32_t)stage[c2 * kSpec + 1];
+            for (uint32_t j = kSpec - 2 + lane; j < cnt; j += 32u) {
+              const Key kk = fcall[(size_t)c2 * kFcCap + 2 + j];
+              atomicAdd(&sh_lvl[(uint32_t)(kk >> lob0) & ((1u << nb0) - 1u)], 1u);
+            }
+          }
+        }
+        __syncthreads();
       }
     }
+    if (fast) {
     // every FC key of every CTA (staged window, then the CTA's extras);
     // fn(key) runs on this warp's lanes
     auto for_fc_keys = [&](uint32_t c2, auto&& fn) {
       const uint32_t cnt = (uint32_t)stage[c2 * kSpec + 1];
       if (lane >= 2 && lane - 2 < cnt) fn(stage[c2 * kSpec + lane]);
-      for (uint32_t j = lane; j + (kSpec - 2) < cnt; j += 32u) fn(sh_fckey[sh_fcoff[c2] + j]);
+      for (uint32_t j = lane; j + (kSpec - 2) < cnt; j += 32u)
+        fn(xg ? fcall[(size_t)c2 * kFcCap + kSpec + j] : sh_fckey[sh_fcoff[c2] + j]);
     };
     uint32_t need = k - G1;
     Key T = (Key)B1 << FS;
@@ -966,7 +996,8 @@ __global__ void __launch_bounds__(kCompressThreads, 1) compress_kernel(const Com
             const uint32_t i = j0 + lane;
             Key kk = T;
             if (i < cnt && !kDirectT)
-              kk = i < kSpec - 2 ? stage[c2 * kSpec + 2 + i] : sh_fckey[sh_fcoff[c2] + i - (kSpec - 2)];
+              kk = i < kSpec - 2 ? stage[c2 * kSpec + 2 + i]
+                   : (xg ? fcall[(size_t)c2 * kFcCap + 2 + i] : sh_fckey[sh_fcoff[c2] + i - (kSpec - 2)]);
             const bool valid = i < cnt;
             const uint32_t v = valid ? ((kk > T ? 0x10000u : 0u) | (kk == T ? 1u : 0u)) : 0u;
             const uint32_t incl = warp_incl_scan(v);
@@ -1033,7 +1064,9 @@ __global__ void __launch_bounds__(kCompressThreads, 1) compress_kernel(const Com
     };
     if (a.idx64 && a.val_f32 && a.val2_out == nullptr) walk(std::true_type{});
     else walk(std::false_type{});
-  } else {
+    }  // fast (no CTA overflowed)
+  }
+  if (!fast) {
     // ================= slow path: many keys share the fine bin B1 =================
     uint32_t need = k - G1;
     Key T = (Key)B1 << FS;

@@ -465,3 +465,21 @@ def test_capped_grid_and_concurrent_streams_identical_frames(cuda, ratio):
         torch.cuda.synchronize()
         for i in range(4):
             assert frames[i].cpu().numpy().tobytes() == expect[i], (rep, i)
+
+
+@pytest.mark.parametrize("layout", ["spread", "clustered"])
+def test_many_final_candidates(cuda, layout):
+    """40,000 distinct values inside one fine histogram bin, with the k-th
+    largest among them.  'spread': every CTA holds a few hundred of them (the
+    fast path, extras read from the CTA regions).  'clustered': one CTA's
+    range holds them all and overflows its region (every CTA falls back to the
+    slow path after B2).  Both must equal the reference selection."""
+    d, hot = 2_500_000, 40_000
+    g = torch.Generator(device=cuda).manual_seed(17)
+    x = torch.rand(d, device=cuda, generator=g) * 0.5
+    vals = 1.0 + torch.rand(hot, device=cuda, generator=g) * 2.0 ** -10
+    pos = (torch.arange(hot, device=cuda) * (d // hot) if layout == "spread"
+           else torch.arange(hot, device=cuda) + 100_000)
+    x[pos] = vals
+    ratio = d / 20_000
+    _check_against_oracle(x, ratio)
