@@ -7,34 +7,39 @@
 // ascending index order.  No sort is performed; the kernel is a radix *select*
 // followed by an index-ordered stream compaction, bit-exact with the reference.
 //
-// One persistent cooperative launch, 1024 threads x one CTA per SM.  The
+// One persistent cooperative launch, 1024 threads x one CTA per SM (or fewer
+// CTAs, gp_topk_compress_*_ctas, so independent compresses share the GPU).  The
 // vector is split into G*32 contiguous "units", one per warp, in index order,
 // so that a warp-ordered compaction of every unit concatenated in unit order
-// is globally index ordered.  A unit is read as 1 KiB rows, one 256-bit load
-// per lane per row (fully coalesced, each lane's 32 bytes contiguous).
+// is globally index ordered.  A unit streams through a per-warp shared-memory
+// ring of two 2 KiB row-pair slots filled by bulk (TMA) copies, one mbarrier
+// per slot; each lane tests two 16-byte pieces of every row.
 //
-//   stage 0  each CTA takes a low watermark lo0 from its own first two rows
-//            (4 keys per lane, no extra traffic): the key whose expected
-//            population is ~k plus a 4-sigma margin.
-//   stage 1  the single full read of x, software-pipelined (4 KiB per warp in
-//            flight): every element with |x| >= lo0 (one FSETP) is a
-//            candidate; candidates go to the warp's index-ordered list (shared
-//            memory, spilling to the workspace) and into an fb-bit "fine"
-//            histogram (smem window, flushed by red.add into one of 8 global
-//            replicas to cut same-address contention).  -- grid barrier B1 --
+//   stage 0  each CTA takes a low watermark lo0 from a sample of its warps'
+//            first rows (4 keys per lane, no extra traffic): the key whose
+//            expected population is ~k plus a 4-sigma margin.
+//   stage 1  the single full read of x: every element with |x| >= lo0 (one
+//            FSETP) is a candidate; candidates go to the warp's index-ordered
+//            list (shared memory, spilling to the workspace) and into an fb-bit
+//            "fine" histogram (smem window starting at the watermark, flushed by
+//            red.add into one of 2 global replicas).  Sparse steps place
+//            candidates with ballots; dense steps with one packed warp scan.
+//            -- grid barrier B1 --
 //   stage 2  every CTA sums the replicas from the top and finds the fine bin
 //            B1 holding the k-th largest key.  If some CTA's watermark sat
 //            above B1, only those CTAs re-stream with a lowered watermark
 //            (one extra barrier; B1 can only move up).  Keys above B1 are kept
-//            ("sure"); keys inside B1 are final candidates (FC).
-//            Fast path (|B1| <= kFcCap): each CTA publishes its FC keys,
-//            index-ordered.  -- grid barrier B2 --
-//   stage 3  every CTA gathers the FC list, resolves the exact threshold key T
-//            and the tie quota by an in-smem radix select over the remaining
-//            low bits (bf16: nothing left, T is B1), derives its own output
-//            offset, and each warp writes its kept (index, value) pairs.
-//   slow path (|B1| > kFcCap) resolves the low bits with global per-level
-//            histograms + barriers, then one more barrier for the tie prefix.
+//            ("sure"); keys inside B1 are final candidates (FC).  Fast path
+//            (<= 64K FC keys): each CTA publishes [sure, |FC|, FC keys].
+//            -- grid barrier B2 --
+//   stage 3  one round trip reads every CTA's first 32 words; the exact
+//            threshold key T and the tie quota come from a radix select over
+//            the unordered FC keys (bf16: T is B1); a CTA's output offset needs
+//            only the earlier CTAs' counts and its own FC keys' tie prefix;
+//            each warp then writes its kept (index, value) pairs.
+//   slow path (too many FC keys, or a CTA overflowing its region) resolves
+//            the low bits with global per-level histograms + barriers, then
+//            one more barrier for the tie prefix.
 //
 // fb (fine-histogram bits) grows with d so |B1| stays small for large tensors.
 // All histogram state is left zeroed for the next call and the grid barrier
@@ -52,7 +57,7 @@
 namespace gp {
 
 constexpr int kMaxGridSpec = 160;      // largest grid: the one-round-trip FC gather stages G*32 keys in smem
-constexpr uint32_t kRing = 4;          // 1 KiB rows in flight per warp (bulk copies into smem)
+constexpr uint32_t kRing = 4;          // 1 KiB rows in flight per warp (two 2-row bulk copies into smem)
 constexpr uint32_t kFcCapBig = 65536;  // final candidates the fast path accepts in total
 #ifndef GP_PREFETCH_ROWS
 #define GP_PREFETCH_ROWS 8
@@ -269,9 +274,6 @@ __device__ __forceinline__ bool warp_cross_desc(const uint32_t* hist, int top, u
 template <class Tr>
 __device__ __forceinline__ void write_out(const CompressArgs& a, uint32_t pos, uint32_t idx, typename Tr::Bits b) {
   using Elem = typename Tr::Elem;
-#ifdef GP_EXP_NOWRITE
-  if (idx != 0xFFFFFFFFu) return;
-#endif
   if (a.idx64) reinterpret_cast<int64_t*>(a.idx_out)[pos] = (int64_t)idx;
   else reinterpret_cast<int32_t*>(a.idx_out)[pos] = (int32_t)idx;
   if (a.val_f32) reinterpret_cast<float*>(a.val_out)[pos] = Tr::to_f32(b);

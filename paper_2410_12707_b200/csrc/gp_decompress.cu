@@ -28,14 +28,8 @@
 namespace gp {
 
 constexpr int kDecThreads = 512;
-#ifndef GP_DEC_BLOCKS
-#define GP_DEC_BLOCKS 4
-#endif
-#ifndef GP_DEC_TILE_KB
-#define GP_DEC_TILE_KB 16
-#endif
-constexpr int kDecBlocksPerSm = GP_DEC_BLOCKS;
-constexpr int kTileBytes = GP_DEC_TILE_KB * 1024;   // smem output tile (double-buffered)
+constexpr int kDecBlocksPerSm = 4;
+constexpr int kTileBytes = 16 * 1024;   // smem output tile (double-buffered)
 constexpr int64_t kMinChunk = 8192;
 #ifndef GP_SPARSE_DENSITY_INV
 #define GP_SPARSE_DENSITY_INV 20
@@ -186,10 +180,6 @@ __global__ void __launch_bounds__(kDecThreads, kDecBlocksPerSm) decompress_kerne
   // (a block count) with no separate search round trip.
   int64_t ci = 0, ni = 0;
   VT cv = VT(0), nv = VT(0);
-#ifdef GP_DEC_DEEP
-  int64_t mi = 0;
-  VT mv = VT(0);
-#endif
   auto fetch = [&](int64_t b, int64_t& i, VT& v) {
     const int64_t j = b + tid;
     if (j >= 0 && j < k) {
@@ -233,9 +223,6 @@ __global__ void __launch_bounds__(kDecThreads, kDecBlocksPerSm) decompress_kerne
   }
   const bool have = fetch(base, ci, cv);
   bool nhave = fetch(base + kDecThreads, ni, nv);
-#ifdef GP_DEC_DEEP
-  bool mhave = fetch(base + 2 * kDecThreads, mi, mv);
-#endif
   bool pend = have && ci >= o0;  // entries below o0 belong to earlier CTAs
   DSTAMP(1);
   const bool vec_ok = ((uintptr_t)out % 16) == 0;
@@ -275,14 +262,7 @@ __global__ void __launch_bounds__(kDecThreads, kDecBlocksPerSm) decompress_kerne
       ci = ni;
       cv = nv;
       pend = nhave;
-#ifdef GP_DEC_DEEP
-      ni = mi;
-      nv = mv;
-      nhave = mhave;
-      mhave = fetch(base + 2 * kDecThreads, mi, mv);
-#else
       nhave = fetch(base + kDecThreads, ni, nv);
-#endif
     }
     if (full) {
       uint4* ov = reinterpret_cast<uint4*>(out + t0);
