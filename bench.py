@@ -195,11 +195,16 @@ def run_ours(args, rank, world, local_rank):
     ws = wss[0]
     load = [0.0] * nstreams
     per_stream = [[] for _ in range(nstreams)]
-    for i in sorted(range(len(units)), key=lambda i: -(units[i]["d"] * (1.6 if units[i]["r"] <= 10 else 1.0))):
+    dense_w = float(os.environ.get("GP_BENCH_DENSE_W", "2.2"))  # relative cost of an r<=10 unit per element (measured)
+
+    def cost(u):
+        return u["d"] * (dense_w if u["r"] <= 10 else 1.0) + float(os.environ.get("GP_BENCH_UNIT_OVH", "4e6"))
+
+    for i in sorted(range(len(units)), key=lambda i: -cost(units[i])):
         j = min(range(nstreams), key=lambda j: load[j])
         units[i]["sj"] = j
         per_stream[j].append(i)
-        load[j] += units[i]["d"] * (1.6 if units[i]["r"] <= 10 else 1.0) + 2e6
+        load[j] += cost(units[i])
     # odd streams run their units smallest-first, so the barrier-bound tails of
     # concurrent kernels do not line up
     if os.environ.get("GP_BENCH_STAGGER", "1") == "1":
