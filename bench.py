@@ -85,9 +85,16 @@ def _ref_pair(args):
 def run_reference(args, rank, world):
     if rank != 0:
         return None
-    # bounded sample of the workload: the smallest boundary (act + grad) at all three ratios
-    sample = [(SHAPES[-1], kind, r) for kind in KINDS for r in RATIOS]
-    cores = min(len(sample), os.cpu_count() or 1)
+    # bounded sample of the workload, one process per host core (np.argsort is
+    # single-threaded): the two smallest boundaries (act + grad) at all three
+    # ratios, padded with more [64,2048,7,7] pairs up to the core count
+    ncpu = os.cpu_count() or 1
+    sample = [(shape, kind, r) for shape in SHAPES[-2:] for kind in KINDS for r in RATIOS]
+    i = 0
+    while len(sample) < ncpu:
+        sample.append((SHAPES[-1], KINDS[i % len(KINDS)], RATIOS[(i // len(KINDS)) % len(RATIOS)]))
+        i += 1
+    cores = min(len(sample), ncpu)
     times = []
     with mp.get_context("spawn").Pool(cores) as pool:
         for step in range(args.warmup + args.steps):
@@ -100,8 +107,9 @@ def run_reference(args, rank, world):
     tot_t = sum(t for t, _ in times)
     tot_b = sum(b for _, b in times)
     value = tot_b / tot_t / 1e9
-    desc = (f"{len(sample)} pairs/step = [64,2048,7,7] activation+gradient x r=10/100/1000, "
-            f"oracle NumPy port (stable argsort), multiprocessing over {cores} cores")
+    desc = (f"{len(sample)} pairs/step = [64,1024,14,14] and [64,2048,7,7] activation+gradient x r=10/100/1000"
+            f"{' (+ more [64,2048,7,7] pairs)' if len(sample) > 12 else ''}, oracle NumPy port (stable argsort), "
+            f"multiprocessing over {cores} of {ncpu} host cores")
     return {
         "impl": "reference", "metric": METRIC, "value": round(value, 4), "unit": "GB/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(1e3 * tot_t / len(times), 2),
