@@ -154,6 +154,22 @@ def two_cluster_link_times(n_stages: int, boundary_bytes: int, fast=(1e-5, 1 / 1
             for s in range(n_stages - 1)]
 
 
+def eq3_pipeline_time(C: list, R: list, n_b: int) -> float:
+    """Eq. 3, planner.py:90-104: sum_d (C_d + R_d) + (n_b - 1) * max_d max(C_d, R_d)."""
+    return sum(c + r for c, r in zip(C, R)) + (n_b - 1) * max(max(c, r) for c, r in zip(C, R))
+
+
+def eq7_pipeline_time(C: list, R: list, n_b: int, base_ratio: float, r_dev: list,
+                      scale_bottleneck_receive: bool = False) -> float:
+    """Eq. 7, planner.py:113-147.  Published closed form: sum_d (C_d + 3 R_d / r_d)
+    + 3 (n_b - 1) * max_d max(C_d, R_d) / r; with scale_bottleneck_receive the
+    bubble is (n_b - 1) * max_d max(C_d, 3 R_d / r_d) (the reference's variant)."""
+    front = sum(c + 3.0 * r / rd for c, r, rd in zip(C, R, r_dev))
+    if scale_bottleneck_receive:
+        return front + max(max(c, 3.0 * r / rd) for c, r, rd in zip(C, R, r_dev)) * (n_b - 1)
+    return front + 3.0 * (n_b - 1) * max(max(c, r) for c, r in zip(C, R)) / base_ratio
+
+
 def measure_link_times(shape, device, reps: int = 5) -> list:
     """Measured dense boundary transfer time (s) of every FP link s -> s+1.
 
@@ -304,6 +320,38 @@ class DistPipeline:
             dist.irecv(buf, src).wait()
         return out if r <= 1.0 else self.codec.decompress(buf, out, r)
 
+    def forward_only(self, tokens: torch.Tensor, targets: torch.Tensor, n_micro: int):
+        """The FP half of a step (fill phase, no backward): what Eq. 3 / Eq. 7 model."""
+        s, S = self.rank, self.S
+        mbs, tgs = tokens.chunk(n_micro), targets.chunk(n_micro)
+        pending = []
+        with torch.no_grad():
+            for m in range(n_micro):
+                inp = mbs[m] if s == 0 else self._recv(s - 1)
+                with torch.autocast("cuda", dtype=torch.bfloat16):
+                    y = self.stage(inp, tgs[m] if s == S - 1 else None)
+                if s < S - 1:
+                    pending.append(self._send(y, s + 1))
+        for w, _buf in pending:
+            w.wait()
+
+    def stage_fp_time(self, tokens: torch.Tensor, targets: torch.Tensor, reps: int = 5) -> float:
+        """C_d: this stage's forward time for one micro-batch (s, CUDA events, median)."""
+        x = tokens[: self.mb] if self.rank == 0 else torch.randn(self.shape, device=self.device)
+        tg = targets[: self.mb] if self.rank == self.S - 1 else None
+        ts = []
+        with torch.no_grad():
+            for _ in range(reps + 1):
+                a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                a.record()
+                with torch.autocast("cuda", dtype=torch.bfloat16):
+                    self.stage(x, tg)
+                b.record()
+                torch.cuda.synchronize()
+                ts.append(a.elapsed_time(b) * 1e-3)
+        ts = sorted(ts[1:])
+        return ts[len(ts) // 2]
+
     def step(self, tokens: torch.Tensor, targets: torch.Tensor, n_micro: int):
         s, S = self.rank, self.S
         mbs, tgs = tokens.chunk(n_micro), targets.chunk(n_micro)
@@ -377,6 +425,9 @@ def run_pipeline(model: str = "medium", plan_mode: str = "uniform", ratio: float
         tt = torch.tensor([t], device=dev)
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         t = float(tt.item())
+    model = None
+    if world > 1 and plan is not None:
+        model = _fp_model_check(pipe, cfg, plan, mb, seq_len, n_micro, ratio, dev, lt if plan_mode == "measured" else None)
     links = {}
     if plan is not None:
         for (s, d), r in sorted(plan.per_link.items()):
@@ -392,9 +443,55 @@ def run_pipeline(model: str = "medium", plan_mode: str = "uniform", ratio: float
             "link_times_s": [round(v, 7) for v in lt] if lt is not None else None,
             "link_times_source": {"measured": "dense boundary P2P, CUDA events, median (measure_link_times)",
                                   "adatopk": "two-cluster alpha-beta model"}.get(plan_mode),
+            "fp_model": model,
             "schedule": "GPipe fill-drain (executor.py:389-404), bf16 autocast, fp32 boundaries",
             "partition": "contiguous equal layers (OP-Fence split of a homogeneous chain)",
             "data": "synthetic tokens, random init"}
+
+
+def _fp_model_check(pipe, cfg, plan, mb, seq_len, n_micro, ratio, dev, link_times=None) -> dict:
+    """The FP (fill) phase measured next to the planner's closed forms, from measured inputs:
+    C_d = each stage's forward time for one micro-batch, R_d = the dense boundary
+    receive time of the link into stage d (R_0 = 0), r_d = the plan's ratio on that link."""
+    world, rank = dist.get_world_size(), dist.get_rank()
+    tok, tgt = synthetic_batch(cfg, mb * n_micro, seq_len, dev, seed=123)
+    c = torch.zeros(world, dtype=torch.float64, device=dev)
+    c[rank] = pipe.stage_fp_time(tok, tgt)
+    dist.all_reduce(c)
+    C = c.tolist()
+    lt = link_times if link_times is not None else measure_link_times((mb, seq_len, cfg.n_embd), dev)
+    R = [0.0] + list(lt)
+    r_dev = [1.0] + [plan.ratio_for(s, s + 1) for s in range(world - 1)]
+
+    def timed_fp(p) -> float:
+        ts = []
+        for _ in range(3):
+            dist.barrier()
+            torch.cuda.synchronize()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record()
+            p.forward_only(tok, tgt, n_micro)
+            b.record()
+            torch.cuda.synchronize()
+            ts.append(a.elapsed_time(b) * 1e-3)
+        tt = torch.tensor([sorted(ts)[1]], device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        return float(tt.item())
+
+    t_comp = timed_fp(pipe)
+    saved = pipe.plan
+    pipe.plan = None  # the same stages with dense boundaries
+    t_dense = timed_fp(pipe)
+    pipe.plan = saved
+    return {"C_stage_fp_s": [round(v, 6) for v in C], "R_link_dense_s": [round(v, 7) for v in R],
+            "r_link": [round(v, 3) for v in r_dev], "n_b": n_micro,
+            "eq3_dense_fp_ms": round(1e3 * eq3_pipeline_time(C, R, n_micro), 3),
+            "measured_dense_fp_ms": round(1e3 * t_dense, 3),
+            "eq7_compressed_fp_ms": round(1e3 * eq7_pipeline_time(C, R, n_micro, ratio, r_dev), 3),
+            "eq7_scaled_bottleneck_fp_ms": round(1e3 * eq7_pipeline_time(C, R, n_micro, ratio, r_dev, True), 3),
+            "measured_compressed_fp_ms": round(1e3 * t_comp, 3),
+            "note": "planner closed forms (planner.py:90-147) from measured C_d / R_d next to the measured fill "
+                    "phase; the reference's DES is out of scope"}
 
 
 def synthetic_batch(cfg: GPT2Config, batch: int, seq_len: int, device, seed: int = 0):
@@ -404,5 +501,6 @@ def synthetic_batch(cfg: GPT2Config, batch: int, seq_len: int, device, seed: int
 
 
 __all__ = ["GPT2Config", "GPT2_SMALL", "GPT2_MEDIUM", "GPT2_XL", "GPT2_TINY", "partition", "make_stage",
-           "link_plan", "two_cluster_link_times", "measure_link_times", "measured_link_plan", "VirtualPipeline", "DistPipeline", "synthetic_batch", "run_pipeline",
+           "link_plan", "two_cluster_link_times", "measure_link_times", "measured_link_plan", "eq3_pipeline_time",
+           "eq7_pipeline_time", "VirtualPipeline", "DistPipeline", "synthetic_batch", "run_pipeline",
            ]

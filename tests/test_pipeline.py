@@ -178,3 +178,29 @@ def test_measured_link_plan_agrees_on_both_ranks(cuda):
     ratios = [r for _, r in res[0][1]]
     assert max(ratios) == 30.0 and all(r >= 1.0 for r in ratios)
     assert res[0][0][0] > 0 and np.isfinite(res[0][2])
+
+
+def test_planner_closed_forms_match_reference():
+    """eq3/eq7 restate planner.py:90-147; checked against hand values and, when
+    the reference is importable (the build container), against its functions."""
+    C, R = [0.010, 0.012, 0.011], [0.0, 0.004, 0.020]
+    n_b, r, r_dev = 8, 100.0, [1.0, 30.0, 300.0]
+    eq3 = sum(c + x for c, x in zip(C, R)) + 7 * 0.020
+    assert PL.eq3_pipeline_time(C, R, n_b) == pytest.approx(eq3, rel=0, abs=0)
+    eq7 = sum(c + 3 * x / q for c, x, q in zip(C, R, r_dev)) + 3 * 7 * 0.020 / r
+    assert PL.eq7_pipeline_time(C, R, n_b, r, r_dev) == pytest.approx(eq7, rel=0, abs=0)
+    ref = "/root/reference/pkg/src"
+    if not os.path.isdir(ref):
+        pytest.skip("reference not mounted")
+    import sys
+    sys.path.insert(0, ref)
+    try:
+        from geopipe import planner as RP
+    finally:
+        sys.path.remove(ref)
+    sc = RP.StageCosts(devices=["a", "b", "c"], compute=dict(zip("abc", C)), receive=dict(zip("abc", R)))
+    assert RP.pipeline_time(sc, n_b) == PL.eq3_pipeline_time(C, R, n_b)
+    assert RP.compressed_pipeline_time(sc, n_b, r, dict(zip("abc", r_dev))) == \
+        PL.eq7_pipeline_time(C, R, n_b, r, r_dev)
+    assert RP.compressed_pipeline_time(sc, n_b, r, dict(zip("abc", r_dev)), scale_bottleneck_receive=True) == \
+        PL.eq7_pipeline_time(C, R, n_b, r, r_dev, scale_bottleneck_receive=True)
