@@ -8,6 +8,7 @@
 //   topk_decompress :97-103   -> gp_topk_decompress / _frame / _unsorted
 //   adatopk_plan    :111-129  -> gp_adatopk_plan (device) / gp_adatopk_plan_host
 //   SparsePayload.to_bytes :39-44 -> the *_frame variants write/read that layout
+#include <atomic>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -18,17 +19,19 @@
 namespace {
 
 int device_info(gp::DeviceInfo* info) {
-  static int cached_sms[64] = {0};
+  // per-device SM count, cached; concurrent first calls from several host
+  // threads store the same value (atomics: no data race)
+  static std::atomic<int> cached_sms[gp::kMaxDevices];
   int dev = 0;
-  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return GP_ERR_CUDA;
-  if (!cached_sms[dev]) {
-    int sms = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= gp::kMaxDevices) return GP_ERR_CUDA;
+  int sms = cached_sms[dev].load(std::memory_order_acquire);
+  if (!sms) {
     if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || sms < 1)
       return GP_ERR_CUDA;
-    cached_sms[dev] = sms;
+    cached_sms[dev].store(sms, std::memory_order_release);
   }
   info->ordinal = dev;
-  info->num_sms = cached_sms[dev];
+  info->num_sms = sms;
   return GP_OK;
 }
 

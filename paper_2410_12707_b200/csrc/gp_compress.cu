@@ -45,6 +45,7 @@
 // All histogram state is left zeroed for the next call and the grid barrier
 // is self-resetting, so the workspace needs to be zeroed only once.
 #include <algorithm>
+#include <atomic>
 #include <cmath>
 #include <type_traits>
 
@@ -1212,20 +1213,21 @@ static int launch_compress_t(CompressArgs a, const DeviceInfo& dev, cudaStream_t
     keep_all_kernel<Tr><<<blocks, 256, 0, stream>>>(a);
     return cudaGetLastError() == cudaSuccess ? 0 : 5;
   }
-  static int configured[64] = {0};
-  static int max_blocks_per_sm[64] = {0};
+  // per-device: the kernel's smem attribute set once and its occupancy (0 =
+  // not yet known); concurrent first calls do the same idempotent setup
+  static std::atomic<int> blocks_per_sm[kMaxDevices];
   const size_t smem = Smem<Tr>::total;
-  if (!configured[dev.ordinal]) {
+  if (dev.ordinal < 0 || dev.ordinal >= kMaxDevices) return 5;
+  int nb = blocks_per_sm[dev.ordinal].load(std::memory_order_acquire);
+  if (!nb) {
     if (cudaFuncSetAttribute(compress_kernel<Tr>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
       return 5;
-    int nb = 0;
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, compress_kernel<Tr>, kCompressThreads, smem) != cudaSuccess ||
         nb < 1)
       return 5;
-    max_blocks_per_sm[dev.ordinal] = nb;
-    configured[dev.ordinal] = 1;
+    blocks_per_sm[dev.ordinal].store(nb, std::memory_order_release);
   }
-  uint32_t gmax = (uint32_t)std::min(dev.num_sms * max_blocks_per_sm[dev.ordinal], kMaxGridSpec);
+  uint32_t gmax = (uint32_t)std::min(dev.num_sms * nb, kMaxGridSpec);
   if (dev.max_ctas > 0) gmax = std::min(gmax, (uint32_t)dev.max_ctas);
   const uint32_t G =
       (uint32_t)std::min<uint64_t>(gmax, std::max<uint64_t>(1, ((uint64_t)a.d + kMinPerCta - 1) / kMinPerCta));

@@ -21,6 +21,7 @@
 // General path (unsorted / repeated indices) reproduces numpy's
 // last-write-wins `out[indices] = values` with an atomicMax "winner" pass.
 #include <algorithm>
+#include <atomic>
 #include <type_traits>
 
 #include "gp_kernels.cuh"
@@ -389,11 +390,14 @@ static int run_fast(const DecompressArgs& a, const DeviceInfo& dev, cudaStream_t
   const int64_t tile_elems = kTileBytes / (int64_t)sizeof(OT);
   chunk = (chunk + tile_elems - 1) / tile_elems * tile_elems;  // whole, 16-byte aligned tiles
   const int64_t grid = (a.d + chunk - 1) / chunk;
-  static bool carveout_set[64] = {false};  // 4 CTAs x 32 KiB per SM needs the max-shared carveout
-  if (!carveout_set[dev.ordinal]) {
-    cudaFuncSetAttribute(decompress_kernel<IT, VT, OT>, cudaFuncAttributePreferredSharedMemoryCarveout,
-                         cudaSharedmemCarveoutMaxShared);
-    carveout_set[dev.ordinal] = true;
+  // 4 CTAs x 32 KiB per SM needs the max-shared carveout (set once per device; idempotent)
+  static std::atomic<bool> carveout_set[kMaxDevices];
+  if (dev.ordinal < 0 || dev.ordinal >= kMaxDevices) return 5;
+  if (!carveout_set[dev.ordinal].load(std::memory_order_acquire)) {
+    if (cudaFuncSetAttribute(decompress_kernel<IT, VT, OT>, cudaFuncAttributePreferredSharedMemoryCarveout,
+                             cudaSharedmemCarveoutMaxShared) != cudaSuccess)
+      return 5;
+    carveout_set[dev.ordinal].store(true, std::memory_order_release);
   }
   if (a.mode == 0 && a.k * kSparseDensityInv <= a.d && a.d * (int64_t)sizeof(OT) <= kSparseMaxBytes) {
     decompress_sparse_kernel<IT, VT, OT><<<(unsigned)grid, kDecThreads, 0, s>>>(

@@ -56,6 +56,8 @@ struct WsLayout {
   size_t ctrl, hist1, hist_lvl, cta_a, cta_b, fcreg, lists, total;
 };
 
+constexpr int kMaxDevices = 64;  // per-device launch configuration caches
+
 struct DeviceInfo {
   int ordinal;
   int num_sms;
