@@ -483,3 +483,75 @@ def test_many_final_candidates(cuda, layout):
     x[pos] = vals
     ratio = d / 20_000
     _check_against_oracle(x, ratio)
+
+
+def _decompress_flags(cuda, idx, vals, d, cases, mode=0):
+    """Run the fast decompress once per case (each case mutates `idx` in place,
+    launches, and undoes the mutation, all stream-ordered) and return the
+    validation flag of every launch."""
+    L = _lib.lib()
+    s = torch.cuda.current_stream().cuda_stream
+    out = torch.zeros(d, device=cuda)
+    err = torch.zeros(len(cases) + 1, dtype=torch.int32, device=cuda)
+    k = idx.numel()
+
+    def launch(slot):
+        assert L.gp_topk_decompress(idx.data_ptr(), 8, vals.data_ptr(), 0, k, d, out.data_ptr(), 0, mode,
+                                    err[slot:].data_ptr(), s) == 0
+
+    launch(0)
+    for c, (kind, j) in enumerate(cases, 1):
+        saved = idx[j:j + 2].clone()
+        if kind == "swap":
+            idx[j:j + 2] = saved.flip(0)
+        else:  # "dup": idx[j+1] = idx[j]
+            idx[j + 1:j + 2] = saved[:1]
+        launch(c)
+        idx[j:j + 2] = saved
+    return err.cpu().numpy()
+
+
+def _sorted_unique(rng, lo, hi, n):
+    return np.sort(rng.choice(np.arange(lo, hi, dtype=np.int64), n, replace=False))
+
+
+@pytest.mark.parametrize("layout", ["uniform", "uniform_accumulate", "clustered", "large", "sparse"])
+def test_decompress_sortedness_flag_is_exact(cuda, layout):
+    """The fast decompress kernels validate strict increase in the same launch
+    (each CTA checks its share of the adjacent pairs).  No false positive on
+    sorted input (it would cost a general re-run), and every single violation
+    is flagged: one adjacent swap or duplicate, placed next to every
+    4096-aligned output position (every possible CTA boundary, where a CTA's
+    entries start) and at random.  Tiled kernel for all layouts but 'sparse'
+    (fill + scatter)."""
+    rng = np.random.default_rng(23)
+    if layout.startswith("uniform"):
+        d = 4 << 20
+        h = _sorted_unique(rng, 0, d, d // 10)
+    elif layout == "clustered":  # two dense clusters, long empty stretches (probe window misses)
+        d = 4 << 20
+        h = np.concatenate([_sorted_unique(rng, 100_000, 400_000, 150_000),
+                            _sorted_unique(rng, 3_000_000, 3_200_000, 150_000)])
+    elif layout == "large":  # > 64 MB output: tiled kernel at r = 100
+        d = 20 << 20
+        h = _sorted_unique(rng, 0, d, d // 100)
+    else:  # k/d = 1/100, 16 MB output: fill + scatter kernel
+        d = 4 << 20
+        h = _sorted_unique(rng, 0, d, d // 100)
+    k = h.size
+    step = 4096 if d <= (4 << 20) else 9 * 4096
+    lbs = np.searchsorted(h, np.arange(step, d, step))
+    pos = set()
+    for lb in lbs:
+        pos.update((int(lb) - 2, int(lb) - 1, int(lb)))
+    pos.update(int(p) for p in rng.integers(0, k - 1, 200))
+    pos.update((0, 1, 510, 511, 512, k - 3, k - 2))
+    pos = sorted(p for p in pos if 0 <= p <= k - 2)
+    cases = [("swap", p) for p in pos] + [("dup", int(p)) for p in rng.choice(pos, 100, replace=False)]
+    idx = torch.from_numpy(h).to(cuda)
+    vals = torch.randn(k, device=cuda)
+    flags = _decompress_flags(cuda, idx, vals, d, cases, mode=1 if layout.endswith("accumulate") else 0)
+    assert flags[0] == 0, "false positive on sorted input"
+    missed = [c for c, f in zip(cases, flags[1:]) if not f & _lib.FLAG_UNSORTED]
+    assert not missed, missed[:10]
+    np.testing.assert_array_equal(idx.cpu().numpy(), h)
