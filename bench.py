@@ -116,7 +116,8 @@ def run_reference(args, rank, world):
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
         "data": "synthetic (seeded ReLU(N(0,1)) activations, N(0,1)*1e-3 gradients)",
         "config": {"workload": WORKLOAD, "sample": desc},
-        "cpu_baseline": {"value": round(value, 4), "unit": "GB/s", "cores": cores, "kind": "port", "sample": desc},
+        "cpu_baseline": {"value": round(value, 4), "unit": "GB/s", "cores": cores, "kind": "port", "sample": desc,
+                         "cpu_count": ncpu, "cpu_model": _cpu_model()},
         "e2e": {"value": round(value, 4), "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
 
@@ -542,6 +543,7 @@ def run_ours(args, rank, world, local_rank):
         line["c1_gpt2_small"] = bench_c1(P, L, dev, flush, peak)
         line["cpu_baseline"] = cpu_baseline()
         line["e2e"] = bench_e2e(P, dev)
+        line["gpu_comparator_torch_topk"] = bench_torch_topk(units, dev, flush)
     elif world > 1:
         line["e2e"] = bench_e2e_dist(P, dev, rank, world)
     if peer:
@@ -721,12 +723,68 @@ def bench_c1(P, L, dev, flush, peak, reps=20):
     return res
 
 
+def bench_torch_topk(units, dev, flush, reps=3):
+    """Informative GPU comparator (the paper's), not a parity path:
+    per pair torch.topk(|x|, k, sorted=False) + index sort + value gather, then a zeroed output and
+    index_copy_.  All of one step's pairs in one CUDA graph on one stream, L2 flushed before each replay."""
+    import torch
+
+    outs = [torch.empty_like(u["x"]) for u in units]
+
+    def step():
+        for u, o in zip(units, outs):
+            x = u["x"]
+            _, i = torch.topk(x.abs(), u["k"], sorted=False)
+            si, _ = torch.sort(i)
+            v = x[si]
+            o.zero_()
+            o.index_copy_(0, si, v)
+
+    side = torch.cuda.Stream(dev)
+    side.wait_stream(torch.cuda.current_stream(dev))
+    with torch.cuda.stream(side):
+        step()  # warm the allocator before capture
+    torch.cuda.synchronize(dev)
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=side):
+        step()
+    ts = []
+    for i in range(reps + 1):
+        flush.sum()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        g.replay()
+        e1.record()
+        e1.synchronize()
+        if i >= 1:
+            ts.append(e0.elapsed_time(e1))
+    ms = statistics.median(ts)
+    b = sum(pair_bytes(u["d"], 4, u["k"]) for u in units)
+    del g, outs
+    torch.cuda.empty_cache()
+    return {"ms_per_step": round(ms, 3), "value": round(b / (ms * 1e-3) / 1e9, 1), "unit": "GB/s",
+            "note": "informative GPU comparator, not parity (tie order may differ): torch.topk(|x|, k, "
+                    "sorted=False) + torch.sort of the indices + gather; decompress zero_ + index_copy_; the step's "
+                    "pairs in one CUDA graph on one stream, L2 flushed before each replay"}
+
+
+def _cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return None
+
+
 def cpu_baseline():
     """The reference algorithm (oracle NumPy port) on one [64,2048,7,7] activation at r=100, 1 core."""
     dt, b = min(_ref_pair((SHAPES[-1], "activation", 100.0, 7)) for _ in range(2))
     return {"value": round(b / dt / 1e9, 4), "unit": "GB/s", "cores": 1, "kind": "port",
             "sample": "1 x [64,2048,7,7] fp32 activation, r=100, compress+decompress, best of 2 "
-                      "(np.argsort(kind='stable') is single-threaded)", "cpu_count": os.cpu_count()}
+                      "(np.argsort(kind='stable') is single-threaded)", "cpu_count": os.cpu_count(),
+            "cpu_model": _cpu_model()}
 
 
 def bench_e2e(P, dev, steps=2):

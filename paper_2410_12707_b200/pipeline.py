@@ -170,6 +170,34 @@ def eq7_pipeline_time(C: list, R: list, n_b: int, base_ratio: float, r_dev: list
     return front + 3.0 * (n_b - 1) * max(max(c, r) for c, r in zip(C, R)) / base_ratio
 
 
+def des_chain_fp_time(C: list, M: list, n_b: int) -> float:
+    """FP makespan of a stage chain under the reference's discrete-event model
+    (simulator.py:108-268, phases=("fp",)): one op at a time per device, one
+    message in flight per directed link (FIFO: a send starts at max(producer
+    finish, link free) and occupies the link for the message time), every FP
+    task of micro-batch m on stage s after its input message arrives.  On a
+    chain each device receives its tasks in micro-batch order, so the event loop
+    reduces to this flow-shop recurrence.  C[s] = stage s's time per
+    micro-batch, M[s] = the message time on the link into stage s (M[0]
+    unused).  tests/test_pipeline.py checks it against the reference's
+    `simulate` on random chains."""
+    S = len(C)
+    dev_free = [0.0] * S
+    link_free = [0.0] * S
+    makespan = 0.0
+    for _ in range(n_b):
+        finish = 0.0
+        for s in range(S):
+            ready = 0.0
+            if s > 0:
+                send = max(finish, link_free[s])
+                link_free[s] = ready = send + M[s]
+            finish = max(ready, dev_free[s]) + C[s]
+            dev_free[s] = finish
+        makespan = max(makespan, finish)
+    return makespan
+
+
 def measure_link_times(shape, device, reps: int = 5) -> list:
     """Measured dense boundary transfer time (s) of every FP link s -> s+1.
 
@@ -478,6 +506,10 @@ def _fp_model_check(pipe, cfg, plan, mb, seq_len, n_micro, ratio, dev, link_time
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         return float(tt.item())
 
+    # the DES charges a compressed message select_k(elems, r) * 12 bytes
+    # (simulator.py:96-105); with measured R_d that is R_d scaled by the byte ratio
+    d_b = mb * seq_len * cfg.n_embd
+    M_comp = [0.0] + [x * (12 * select_k(d_b, q) / (4 * d_b)) if q > 1.0 else x for x, q in zip(R[1:], r_dev[1:])]
     t_comp = timed_fp(pipe)
     saved = pipe.plan
     pipe.plan = None  # the same stages with dense boundaries
@@ -490,8 +522,11 @@ def _fp_model_check(pipe, cfg, plan, mb, seq_len, n_micro, ratio, dev, link_time
             "eq7_compressed_fp_ms": round(1e3 * eq7_pipeline_time(C, R, n_micro, ratio, r_dev), 3),
             "eq7_scaled_bottleneck_fp_ms": round(1e3 * eq7_pipeline_time(C, R, n_micro, ratio, r_dev, True), 3),
             "measured_compressed_fp_ms": round(1e3 * t_comp, 3),
-            "note": "planner closed forms (planner.py:90-147) from measured C_d / R_d next to the measured fill "
-                    "phase; the reference's DES is out of scope"}
+            "des_dense_fp_ms": round(1e3 * des_chain_fp_time(C, R, n_micro), 3),
+            "des_compressed_fp_ms": round(1e3 * des_chain_fp_time(C, M_comp, n_micro), 3),
+            "note": "planner closed forms (planner.py:90-147) and the reference's discrete-event model "
+                    "(simulator.py:108-268, restated for a chain: des_chain_fp_time) from measured C_d / R_d, next "
+                    "to the measured fill phase; neither model charges the compress/decompress kernels"}
 
 
 def synthetic_batch(cfg: GPT2Config, batch: int, seq_len: int, device, seed: int = 0):
@@ -502,5 +537,5 @@ def synthetic_batch(cfg: GPT2Config, batch: int, seq_len: int, device, seed: int
 
 __all__ = ["GPT2Config", "GPT2_SMALL", "GPT2_MEDIUM", "GPT2_XL", "GPT2_TINY", "partition", "make_stage",
            "link_plan", "two_cluster_link_times", "measure_link_times", "measured_link_plan", "eq3_pipeline_time",
-           "eq7_pipeline_time", "VirtualPipeline", "DistPipeline", "synthetic_batch", "run_pipeline",
+           "eq7_pipeline_time", "des_chain_fp_time", "VirtualPipeline", "DistPipeline", "synthetic_batch", "run_pipeline",
            ]

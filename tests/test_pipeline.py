@@ -204,3 +204,47 @@ def test_planner_closed_forms_match_reference():
         PL.eq7_pipeline_time(C, R, n_b, r, r_dev)
     assert RP.compressed_pipeline_time(sc, n_b, r, dict(zip("abc", r_dev)), scale_bottleneck_receive=True) == \
         PL.eq7_pipeline_time(C, R, n_b, r, r_dev, scale_bottleneck_receive=True)
+
+
+def test_des_chain_matches_reference_simulator():
+    """des_chain_fp_time restates simulator.simulate (FP phase) for a stage
+    chain; checked against hand values and, when the reference is importable,
+    against its event loop on random heterogeneous chains (exact equality:
+    beta = 1e-300 makes the reference's message time exactly alpha)."""
+    import random
+
+    # hand case (tests/test_simulator.py:37-45 of the reference): C = 2, message 1, 3 micro-batches -> 9
+    assert PL.des_chain_fp_time([2.0, 2.0], [0.0, 1.0], 3) == 9.0
+    # link-bound chain: messages serialise on the link
+    assert PL.des_chain_fp_time([1.0, 1.0], [0.0, 3.0], 4) == 1.0 + 4 * 3.0 + 1.0
+    ref = "/root/reference/pkg/src"
+    if not os.path.isdir(ref):
+        pytest.skip("reference not mounted")
+    import sys
+    sys.path.insert(0, ref)
+    try:
+        from geopipe.costmodel import DeviceProfile, LinkProfile, NetworkGraph, OpCost
+        from geopipe.opdag import build_dag
+        from geopipe.opfence import Schedule
+        from geopipe.simulator import simulate
+    finally:
+        sys.path.remove(ref)
+    rng = random.Random(7)
+    for trial in range(60):
+        S, n_b = rng.randint(2, 6), rng.randint(1, 9)
+        C = [rng.uniform(0.5, 3.0) for _ in range(S)]
+        M = [0.0] + [rng.choice([0.0, rng.uniform(0.1, 4.0)]) for _ in range(S - 1)]
+        specs = [dict(name="in", kind="input", attrs={"size": 8})]
+        for s in range(S):
+            specs.append(dict(name=f"op{s}", kind="relu", args=("in" if s == 0 else f"op{s - 1}",),
+                              attrs={"size": 8}))
+        dag = build_dag(specs)
+        devs = [DeviceProfile(device_id=f"d{s}", peak_flops=1.0) for s in range(S)]
+        links = {(f"d{s - 1}", f"d{s}"): LinkProfile(src=f"d{s - 1}", dst=f"d{s}", alpha=M[s], beta=1e-300)
+                 for s in range(1, S)}
+        net = NetworkGraph(devices=devs, links=links)
+        sched = Schedule(assignment={"in": "d0", **{f"op{s}": f"d{s}" for s in range(S)}})
+        costs = {"in": OpCost(flops=0.0, out_bytes=32.0), **{f"op{s}": OpCost(flops=C[s], out_bytes=32.0)
+                                                              for s in range(S)}}
+        tr = simulate(dag, sched, costs, net, n_b=n_b)
+        assert PL.des_chain_fp_time(C, M, n_b) == tr.makespan_fp, (trial, S, n_b)
