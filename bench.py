@@ -228,8 +228,9 @@ def run_ours(args, rank, world, local_rank):
     flush = torch.ones(128 << 20, dtype=torch.float32, device=dev)  # 512 MB read between steps
     step_bytes = sum(pair_bytes(u["d"], 4, u["k"]) for u in units)
 
-    def compress(u):  # on the current stream (the capture stream while a graph is recorded)
-        st = L.gp_topk_compress_frame_ctas(u["x"].data_ptr(), 0, u["d"], u["k"], u["frame"].data_ptr(),
+    def compress(u, dst=None):  # on the current stream (the capture stream while a graph is recorded)
+        st = L.gp_topk_compress_frame_ctas(u["x"].data_ptr(), 0, u["d"], u["k"],
+                                           u["frame"].data_ptr() if dst is None else dst,
                                            wss[u["sj"]].data_ptr(), wsb, torch.cuda.current_stream(dev).cuda_stream,
                                            ctas)
         assert st == 0, st
@@ -239,11 +240,15 @@ def run_ours(args, rank, world, local_rank):
                                         err.data_ptr(), torch.cuda.current_stream(dev).cuda_stream)
         assert st == 0, st
 
-    # N>1 transport: "peer" = frames copied by the copy engines into the
-    # successor's receive buffer (CUDA IPC over NVLink, overlapping the next
-    # compress) and signalled with interprocess events; "nccl" = one
-    # batch_isend_irecv of all frames after the compress phase.
-    peer = world > 1 and args.transport == "peer"
+    # N>1 transport: "peer" = frames written locally, then copied by the copy
+    # engines into the successor's receive buffer (CUDA IPC over NVLink,
+    # overlapping the next compress); "peer-store" = the compress kernel
+    # stores each frame straight into that buffer (the send fused into the
+    # producing kernel; measured slower); both hand off with
+    # interprocess events.  "nccl" = one batch_isend_irecv of all frames after
+    # the compress phase.
+    peer = world > 1 and args.transport in ("peer", "peer-store")
+    direct = peer and args.transport == "peer-store"
     ring = copy_streams = cpu_group = None
     if peer:
         from paper_2410_12707_b200.peer import PeerRing
@@ -285,17 +290,17 @@ def run_ours(args, rank, world, local_rank):
         def body(i, u, st):
             if ev is not None:
                 ev[i][0].record(st)
-            compress(u)
+            compress(u, ring.peer_recv(parity) + u["off"] if direct else None)
             if ev is not None:
                 ev[i][1].record(st)
-            if peer:  # frame i travels while the next frames are being compressed
+            if peer and not direct:  # frame i travels while the next frames are being compressed
                 cs = copy_streams[u["sj"]]
                 done = torch.cuda.Event()
                 done.record(st)
                 cs.wait_event(done)
                 ring.copy(ring.peer_recv(parity) + u["off"], u["frame"].data_ptr(), 16 + 12 * u["k"], cs)
         on_streams(body)
-        if peer:
+        if peer and not direct:
             for cs in copy_streams:
                 torch.cuda.current_stream(dev).wait_stream(cs)
 
@@ -477,7 +482,9 @@ def run_ours(args, rank, world, local_rank):
                    "kernel_times": "per-launch CUDA events from separate eager steps (roofline, per_config)",
                    "parallelism": ("replicas, no exchange" if world == 1 else
                                    f"{world} ranks, compressed frames ring-exchanged "
-                                   + ("by copy engines into the successor's buffer over NVLink (CUDA IPC, "
+                                   + ("by the compress kernel's own stores into the successor's buffer over "
+                                      "NVLink (CUDA IPC peer memory; interprocess-event handoff)" if direct else
+                                      "by copy engines into the successor's buffer over NVLink (CUDA IPC, "
                                       "overlapping the next compress; interprocess-event handoff)" if peer else
                                       "over NCCL P2P (batch_isend_irecv)"))},
         "roofline": {"bound": "hbm", "kernel": "compress_kernel<f32> (cooperative, 1 CTA/SM)",
@@ -838,9 +845,9 @@ def main():
     ap.add_argument("--no-graph", action="store_true", help="timed steps as eager launches (no CUDA graphs)")
     ap.add_argument("--streams", type=int, default=4,
                     help="concurrent streams for the independent units (compress grid = num_sms / streams)")
-    ap.add_argument("--transport", default="peer", choices=["peer", "nccl"],
+    ap.add_argument("--transport", default="peer", choices=["peer", "peer-store", "nccl"],
                     help="N>1 frame exchange: copy engines into the successor's buffer over NVLink (CUDA IPC), "
-                         "or NCCL batch_isend_irecv")
+                         "the compress kernel's own stores there, or NCCL batch_isend_irecv")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-pipeline", action="store_true", help="skip the GPT-2 pipeline sub-measurement")
     args = ap.parse_args()
