@@ -587,12 +587,20 @@ def run_ours(args, rank, world, local_rank):
     if not args.no_pipeline:
         from paper_2410_12707_b200 import pipeline as PL
 
-        line["pipeline"] = PL.run_pipeline("medium", "uniform", 100.0, n_micro=8, steps=3, warmup=2)
+        def sub(key, *a, **kw):
+            # informative sub-objects: a (rank-symmetric) failure is recorded, not fatal to the line
+            try:
+                line[key] = PL.run_pipeline(*a, **kw)
+            except Exception as exc:  # noqa: BLE001
+                line[key] = {"error": f"{type(exc).__name__}: {exc}"[:300]}
+                torch.cuda.empty_cache()
+
+        sub("pipeline", "medium", "uniform", 100.0, n_micro=8, steps=3, warmup=2)
         if world > 1:  # Eq. 6 on the device from measured link times
-            line["pipeline_measured_adatopk"] = PL.run_pipeline("medium", "measured", 100.0, n_micro=8, steps=3,
-                                                                warmup=1)
-        if world == 8:  # configs[3]: GPT-2 XL, 8 stages, Eq. 6 ratios from a two-cluster link model
-            line["pipeline_xl_adatopk"] = PL.run_pipeline("xl", "adatopk", 100.0, steps=2, warmup=1)
+            sub("pipeline_measured_adatopk", "medium", "measured", 100.0, n_micro=8, steps=3, warmup=2)
+        if world == 8 or (world > 1 and os.environ.get("GP_BENCH_XL")):
+            # configs[3]: GPT-2 XL, 8 stages, Eq. 6 ratios from a two-cluster link model
+            sub("pipeline_xl_adatopk", "xl", "adatopk", 100.0, steps=3, warmup=2)
     return line
 
 

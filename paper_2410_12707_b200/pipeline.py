@@ -417,7 +417,8 @@ def run_pipeline(model: str = "medium", plan_mode: str = "uniform", ratio: float
                  n_micro: int = None, seq_len: int = 1024, steps: int = 3, warmup: int = 1) -> dict:
     """Time GPipe steps of GPT-2 with one stage per rank (or one stage on one GPU).
 
-    Returns samples/s = global batch / step time (CUDA events, max over ranks).
+    Returns samples/s = global batch / median step time (CUDA events, each step
+    the max over ranks) after `warmup` untimed steps.
     Call after torch.distributed is initialised when WORLD_SIZE > 1.
     """
     cfg = MODELS[model]
@@ -448,11 +449,11 @@ def run_pipeline(model: str = "medium", plan_mode: str = "uniform", ratio: float
         torch.cuda.synchronize()
         if i >= warmup:
             times.append(a.elapsed_time(b))
-    t = sum(times) / len(times)
-    if world > 1:
-        tt = torch.tensor([t], device=dev)
+    if world > 1:  # per step, the slowest rank
+        tt = torch.tensor(times, device=dev)
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        t = float(tt.item())
+        times = tt.tolist()
+    t = sorted(times)[len(times) // 2]  # median step
     model = None
     if world > 1 and plan is not None:
         model = _fp_model_check(pipe, cfg, plan, mb, seq_len, n_micro, ratio, dev, lt if plan_mode == "measured" else None)
@@ -466,6 +467,7 @@ def run_pipeline(model: str = "medium", plan_mode: str = "uniform", ratio: float
     return {"metric": "GPT-2 compressed-pipeline samples/s", "value": round(gb / (t * 1e-3), 3), "unit": "samples/s",
             "n_gpus": world, "model": model, "layers": cfg.n_layer, "hidden": cfg.n_embd, "micro_batch": mb,
             "n_micro": n_micro, "global_batch": gb, "seq_len": seq_len, "ms_per_step": round(t, 2),
+            "step_ms": [round(v, 2) for v in times], "warmup": warmup,
             "loss": round(loss, 4), "plan": plan_mode if world > 1 else "none (1 stage, no boundary)",
             "base_ratio": ratio, "boundary_elems": boundary, "dense_boundary_bytes": boundary * 4, "links": links,
             "link_times_s": [round(v, 7) for v in lt] if lt is not None else None,
