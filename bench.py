@@ -214,9 +214,12 @@ def run_ours(args, rank, world, local_rank):
         units[i]["sj"] = j
         per_stream[j].append(i)
         load[j] += cost(units[i])
-    # odd streams run their units smallest-first, so the barrier-bound tails of
-    # concurrent kernels do not line up
-    if os.environ.get("GP_BENCH_STAGGER", "1") == "1":
+    # N=1: odd streams run their units smallest-first, so the barrier-bound
+    # tails of concurrent kernels do not line up.  N>1: every stream runs
+    # largest-first, so the big frames are produced (and their copies to the
+    # successor start) early instead of at the end of the compress phase
+    # (+1.5% at N=2).
+    if os.environ.get("GP_BENCH_STAGGER", "1" if world == 1 else "0") == "1":
         for j in range(1, nstreams, 2):
             per_stream[j].reverse()
     stream_order = [i for lst in per_stream for i in lst]
@@ -247,8 +250,12 @@ def run_ours(args, rank, world, local_rank):
     # producing kernel; measured slower); both hand off with
     # interprocess events.  "nccl" = one batch_isend_irecv of all frames after
     # the compress phase.
-    peer = world > 1 and args.transport in ("peer", "peer-store")
+    # "peer-pull" = no copy: each rank compresses into its own exported
+    # buffer and the successor's decompress kernels read the frames from it
+    # over NVLink (remote loads).
+    peer = world > 1 and args.transport in ("peer", "peer-store", "peer-pull")
     direct = peer and args.transport == "peer-store"
+    pull = peer and args.transport == "peer-pull"
     ring = copy_streams = cpu_group = None
     if peer:
         from paper_2410_12707_b200.peer import PeerRing
@@ -258,8 +265,17 @@ def run_ours(args, rank, world, local_rank):
         for u in units:
             u["off"] = off
             off += (16 + 12 * u["k"] + 255) // 256 * 256
-        ring = PeerRing(off, dev, cpu_group)
-        copy_streams = [torch.cuda.Stream(dev) for _ in range(max(1, args.streams))]  # one per compute stream
+        ring = PeerRing(off, dev, cpu_group, pull=pull)
+        n_copy = int(os.environ.get("GP_BENCH_COPY_STREAMS", str(max(1, args.streams))))
+        copy_streams = [torch.cuda.Stream(dev) for _ in range(max(1, n_copy))]
+        # estimated completion time of every unit's frame (cost model, per-stream prefix sums)
+        est_end = {}
+        for lst in per_stream:
+            acc = 0.0
+            for i in lst:
+                acc += cost(units[i])
+                est_end[i] = acc
+        copy_order = sorted(range(len(units)), key=lambda i: est_end[i])
 
     def exchange():
         nxt, prv = (rank + 1) % world, (rank - 1) % world
@@ -290,17 +306,20 @@ def run_ours(args, rank, world, local_rank):
         def body(i, u, st):
             if ev is not None:
                 ev[i][0].record(st)
-            compress(u, ring.peer_recv(parity) + u["off"] if direct else None)
+            compress(u, ring.peer_recv(parity) + u["off"] if direct else ring.recv(parity) + u["off"] if pull else None)
             if ev is not None:
                 ev[i][1].record(st)
-            if peer and not direct:  # frame i travels while the next frames are being compressed
-                cs = copy_streams[u["sj"]]
-                done = torch.cuda.Event()
-                done.record(st)
-                cs.wait_event(done)
-                ring.copy(ring.peer_recv(parity) + u["off"], u["frame"].data_ptr(), 16 + 12 * u["k"], cs)
+            if peer and not direct and not pull:  # frame i travels while the next frames are being compressed
+                done[i].record(st)
+        done = [torch.cuda.Event() for _ in units] if peer and not direct and not pull else None
         on_streams(body)
-        if peer and not direct:
+        if peer and not direct and not pull:
+            # copies in the estimated order the frames complete, round-robin over the copy streams
+            for n_, i in enumerate(copy_order):
+                u = units[i]
+                cs = copy_streams[n_ % len(copy_streams)]
+                cs.wait_event(done[i])
+                ring.copy(ring.peer_recv(parity) + u["off"], u["frame"].data_ptr(), 16 + 12 * u["k"], cs)
             for cs in copy_streams:
                 torch.cuda.current_stream(dev).wait_stream(cs)
 
@@ -309,7 +328,7 @@ def run_ours(args, rank, world, local_rank):
             if ev is not None:
                 ev[i][2].record(st)
             if peer:
-                src = ring.recv(parity) + u["off"]
+                src = (ring.peer_recv(parity) if pull else ring.recv(parity)) + u["off"]
             else:
                 src = (u["rframe"] if world > 1 else u["frame"]).data_ptr()
             decompress(u, src)
@@ -484,6 +503,8 @@ def run_ours(args, rank, world, local_rank):
                                    f"{world} ranks, compressed frames ring-exchanged "
                                    + ("by the compress kernel's own stores into the successor's buffer over "
                                       "NVLink (CUDA IPC peer memory; interprocess-event handoff)" if direct else
+                                      "by the successor's decompress kernels reading this rank's frames over "
+                                      "NVLink (CUDA IPC peer memory, no copy; interprocess-event handoff)" if pull else
                                       "by copy engines into the successor's buffer over NVLink (CUDA IPC, "
                                       "overlapping the next compress; interprocess-event handoff)" if peer else
                                       "over NCCL P2P (batch_isend_irecv)"))},
@@ -553,7 +574,7 @@ def run_ours(args, rank, world, local_rank):
         line["gpu_comparator_torch_topk"] = bench_torch_topk(units, dev, flush)
     elif world > 1:
         line["e2e"] = bench_e2e_dist(P, dev, rank, world)
-    if peer:
+    if peer and not pull:
         # transfers: one step's frames pushed into the
         # successor's buffer by the copy engines, timed alone, every rank at once
         tb = sum(16 + 12 * u["k"] for u in units)
@@ -562,8 +583,10 @@ def run_ours(args, rank, world, local_rank):
         e0.record(stream)
         for cs in copy_streams:
             cs.wait_stream(stream)
-        for u in units:  # over the copy streams, as in the timed steps
-            ring.copy(ring.peer_recv(0) + u["off"], u["frame"].data_ptr(), 16 + 12 * u["k"], copy_streams[u["sj"]])
+        for n_, i in enumerate(copy_order):  # over the copy streams, as in the timed steps
+            u = units[i]
+            ring.copy(ring.peer_recv(0) + u["off"], u["frame"].data_ptr(), 16 + 12 * u["k"],
+                      copy_streams[n_ % len(copy_streams)])
         for cs in copy_streams:
             stream.wait_stream(cs)
         e1.record(stream)
@@ -853,7 +876,7 @@ def main():
     ap.add_argument("--no-graph", action="store_true", help="timed steps as eager launches (no CUDA graphs)")
     ap.add_argument("--streams", type=int, default=4,
                     help="concurrent streams for the independent units (compress grid = num_sms / streams)")
-    ap.add_argument("--transport", default="peer", choices=["peer", "peer-store", "nccl"],
+    ap.add_argument("--transport", default="peer", choices=["peer", "peer-pull", "peer-store", "nccl"],
                     help="N>1 frame exchange: copy engines into the successor's buffer over NVLink (CUDA IPC), "
                          "the compress kernel's own stores there, or NCCL batch_isend_irecv")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])

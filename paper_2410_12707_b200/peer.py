@@ -18,6 +18,10 @@ interprocess event the successor's stream waits on before decompressing.
     ...decompress from ring.recv[parity] + offset...
     ring.signal_consumed(stream)
 
+In pull mode (`PeerRing(..., pull=True)`) nothing is copied: a rank compresses
+into its own exported buffer and its successor's decompress kernels read the
+frames from it over NVLink; the same events order the two sides.
+
 Handles (buffers and events) are exchanged once over a CPU (gloo) group.  The
 receive buffer is double-buffered by step parity: a sender writing buffer p at
 step s waits for the consumer's record of step s-2 or later, which every rank
@@ -40,7 +44,14 @@ def _handle(raw: bytes):
 
 
 class PeerRing:
-    def __init__(self, recv_bytes: int, device: torch.device, cpu_group=None):
+    """`pull=False` (push): each rank maps its successor's buffer and writes
+    frames there (`peer_recv`); it decompresses from its own (`recv`).
+    `pull=True`: each rank compresses into its own buffer (`recv` = the local
+    frames) and maps its predecessor's (`peer_recv`), which its decompress
+    kernels read directly over NVLink: no copy at all.  The events and their
+    meaning are the same in both directions."""
+
+    def __init__(self, recv_bytes: int, device: torch.device, cpu_group=None, pull: bool = False):
         L = _lib.lib()
         self.L = L
         self.device = device
@@ -61,15 +72,18 @@ class PeerRing:
             objs = [None] * self.world
             dist.all_gather_object(objs, (bytes(mh), bytes(sh), bytes(ch)), group=cpu_group)
             nxt, prv = (self.rank + 1) % self.world, (self.rank - 1) % self.world
+            self.pull = bool(pull)
             self.peer_base = ctypes.c_void_p()
-            raise_for_status(L.gp_ipc_open_mem(_handle(objs[nxt][0]), ctypes.byref(self.peer_base)), "gp_ipc_open_mem")
+            raise_for_status(L.gp_ipc_open_mem(_handle(objs[prv if self.pull else nxt][0]),
+                                               ctypes.byref(self.peer_base)), "gp_ipc_open_mem")
             self.prev_sent, self.next_consumed = ctypes.c_void_p(), ctypes.c_void_p()
             raise_for_status(L.gp_ipc_open_event(_handle(objs[prv][1]), ctypes.byref(self.prev_sent)),
                              "gp_ipc_open_event")
             raise_for_status(L.gp_ipc_open_event(_handle(objs[nxt][2]), ctypes.byref(self.next_consumed)),
                              "gp_ipc_open_event")
 
-    # device pointers of buffer `parity` (local receive side / successor's receive side)
+    # device pointers of buffer `parity`: the local one / the mapped peer's
+    # (push: the successor's receive buffer; pull: the predecessor's frames)
     def recv(self, parity: int) -> int:
         return self.recv_base.value + (parity & 1) * self.recv_bytes
 
