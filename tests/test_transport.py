@@ -120,8 +120,10 @@ def test_ring_exchange_nccl_world2(cuda):
     assert res == {0: True, 1: True}, res
 
 
-def _peer_worker(rank, world, port, q):
-    """Frames through PeerRing (copy engines into the successor's IPC buffer, event handoff)."""
+def _peer_worker(rank, world, port, q, pull=False):
+    """Frames through PeerRing: push = copy engines into the successor's IPC
+    buffer; pull = compress into the own exported buffer, the successor's
+    decompress reads it over NVLink.  Event handoff either way."""
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     try:
         import ctypes
@@ -138,7 +140,7 @@ def _peer_worker(rank, world, port, q):
         d, r = 300_007, 50.0
         k = P.select_k(d, r)
         fb = 16 + 12 * k
-        ring = PeerRing(fb, dev, cpu)
+        ring = PeerRing(fb, dev, cpu, pull=pull)
         st = torch.cuda.current_stream(dev)
         cs = torch.cuda.Stream(dev)
         out = torch.empty(d, device=dev)
@@ -150,19 +152,22 @@ def _peer_worker(rank, world, port, q):
             frame = torch.empty(fb, dtype=torch.uint8, device=dev)
             wsb = L.gp_topk_workspace_bytes(d, 0)
             ws = torch.zeros(wsb, dtype=torch.uint8, device=dev)
-            assert L.gp_topk_compress_frame(x.data_ptr(), 0, d, k, frame.data_ptr(), ws.data_ptr(), wsb,
-                                            st.cuda_stream) == 0
-            ring.wait_consumed(cs)
-            done = torch.cuda.Event()
-            done.record(st)
-            cs.wait_event(done)
-            ring.copy(ring.peer_recv(rnd), frame.data_ptr(), fb, cs)
-            st.wait_stream(cs)
+            if pull:  # the successor must be done with this parity before it is overwritten
+                ring.wait_consumed(st)
+            dst = ring.recv(rnd) if pull else frame.data_ptr()
+            assert L.gp_topk_compress_frame(x.data_ptr(), 0, d, k, dst, ws.data_ptr(), wsb, st.cuda_stream) == 0
+            if not pull:
+                ring.wait_consumed(cs)
+                done = torch.cuda.Event()
+                done.record(st)
+                cs.wait_event(done)
+                ring.copy(ring.peer_recv(rnd), frame.data_ptr(), fb, cs)
+                st.wait_stream(cs)
             ring.signal_sent(st)
             dist.barrier(group=cpu)
             ring.wait_sent(st)
-            assert L.gp_topk_decompress_frame(ring.recv(rnd), k, d, out.data_ptr(), 0, 0, err.data_ptr(),
-                                              st.cuda_stream) == 0
+            src = ring.peer_recv(rnd) if pull else ring.recv(rnd)
+            assert L.gp_topk_decompress_frame(src, k, d, out.data_ptr(), 0, 0, err.data_ptr(), st.cuda_stream) == 0
             ring.signal_consumed(st)
             torch.cuda.synchronize(dev)
             prv = (rank - 1) % world
@@ -179,13 +184,14 @@ def _peer_worker(rank, world, port, q):
 
 
 @pytest.mark.gpu
-def test_peer_ring_world2(cuda):
+@pytest.mark.parametrize("pull", [False, True], ids=["push", "pull"])
+def test_peer_ring_world2(cuda, pull):
     if torch.cuda.device_count() < 2:
         pytest.skip("needs 2 GPUs (run under gpurun --gpus 2)")
     ctx = tmp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    ps = [ctx.Process(target=_peer_worker, args=(r, 2, port, q)) for r in range(2)]
+    ps = [ctx.Process(target=_peer_worker, args=(r, 2, port, q, pull)) for r in range(2)]
     for p in ps:
         p.start()
     res = dict(q.get(timeout=300) for _ in range(2))
