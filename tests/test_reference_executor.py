@@ -123,3 +123,38 @@ def test_host_binding_raises_reference_exceptions(cuda):
         np.testing.assert_array_equal(out, [0, 0, 0, 0, 4, 5, 6, 7])
     finally:
         undo()
+
+
+def test_host_binding_translates_exceptions_cpu():
+    """patch_executor's wrappers re-raise the four compressor exceptions as the
+    given errors module's classes (CPU: stub compressor, fake modules)."""
+    import types
+
+    from paper_2410_12707_b200 import errors as E
+    from paper_2410_12707_b200 import host_binding
+
+    class RefBase(Exception):
+        pass
+
+    ref_errors = types.SimpleNamespace(**{n: type(n, (RefBase,), {}) for n in
+                                          ("InvalidRatio", "EmptyVector", "IndexOutOfRange", "NoCommunication")})
+    raised = {}
+
+    def make(exc):
+        def fn(*a, **kw):
+            raise exc("boom")
+        return fn
+
+    for name in ("InvalidRatio", "EmptyVector", "IndexOutOfRange"):
+        wrapped = host_binding._translate(ref_errors)(make(getattr(E, name)))
+        with pytest.raises(getattr(ref_errors, name)) as ei:
+            wrapped(1)
+        raised[name] = ei.value
+        assert isinstance(ei.value.__cause__, getattr(E, name))
+    with pytest.raises(ValueError):  # anything else passes through untouched
+        host_binding._translate(ref_errors)(make(ValueError))()
+    ex = types.SimpleNamespace(topk_compress="c", topk_decompress="d")
+    undo = host_binding.patch_executor(ex, ref_errors)
+    assert callable(ex.topk_compress) and callable(ex.topk_decompress)
+    undo()
+    assert (ex.topk_compress, ex.topk_decompress) == ("c", "d")
