@@ -10,9 +10,9 @@ gradients go backward as AdaTopK wire frames produced by the sm_100a kernels
 `uniform_plan`.  Stage compute is plain PyTorch (bf16 autocast matmuls, fp32
 residual stream, so boundary tensors are fp32).
 
-The partition is contiguous and equal in layers — what OP-Fence's
-proportional split (opfence.py:412-424) yields for a homogeneous chain of
-identical blocks.  `virtual_stages` runs S stages inside one process (one GPU)
+The partition is OP-Fence's contiguous FLOP-proportional split
+(opfence.py:285-315,412-424) of the operator chain [embeddings, blocks, LM
+head] over identical devices, so the stage holding the head gets fewer blocks.  `virtual_stages` runs S stages inside one process (one GPU)
 with the same compress/decompress at every boundary; it is used for the loss
 parity test against the CPU oracle codec and as the N=1 point.
 """
@@ -100,7 +100,11 @@ class Stage(nn.Module):
         if last:
             torch.manual_seed(seed * 7919 + 2)
             self.ln_f = nn.LayerNorm(cfg.n_embd)
-            self.head = nn.Linear(cfg.n_embd, cfg.vocab, bias=False)
+            # the head GEMM's N padded to a multiple of 64 (GPT-2's 50257 makes
+            # the bf16 GEMM 11x slower on B200: 7.5 vs 0.66 ms, scripts/head_probe.py);
+            # the extra logits are sliced off before the loss, so the model is unchanged
+            self.vocab = cfg.vocab
+            self.head = nn.Linear(cfg.n_embd, (cfg.vocab + 63) // 64 * 64, bias=False)
 
     def forward(self, x, targets=None):
         if self.first:
@@ -109,19 +113,67 @@ class Stage(nn.Module):
         for blk in self.blocks:
             x = blk(x)
         if self.last:
-            logits = self.head(self.ln_f(x)).float()
-            return F.cross_entropy(logits.view(-1, logits.shape[-1]), targets.view(-1))
+            logits = self.head(self.ln_f(x))[..., :self.vocab].float()
+            return F.cross_entropy(logits.reshape(-1, self.vocab), targets.reshape(-1))
         return x
 
 
-def partition(n_layer: int, n_stages: int):
-    """Contiguous, equal split of the layer chain (OP-Fence on a homogeneous chain)."""
-    bounds = [round(i * n_layer / n_stages) for i in range(n_stages + 1)]
-    return [(bounds[i], bounds[i + 1]) for i in range(n_stages)]
+def op_flops(cfg: GPT2Config) -> tuple:
+    """Forward FLOPs per token of one transformer block and of the LM head (the
+    per-operator workload estimate the split is weighted by): a block's four
+    projections (12 h^2 weights, 2 FLOPs each) plus attention (4 T h); the head
+    2 h V."""
+    h = cfg.n_embd
+    return 24.0 * h * h + 4.0 * cfg.n_ctx * h, 2.0 * h * cfg.vocab
+
+
+def proportional_split(weights: list, n_blocks: int) -> list:
+    """Contiguous split of items with `weights` into n_blocks blocks of ~equal
+    load: OP-Fence's greedy rule (opfence.py:285-315, equal shares for identical
+    devices).  Block j closes once its cumulative load reaches (j+1)/n of the
+    total, or earlier when half of the next item's load would overshoot that
+    target; every block gets at least one item.  Returns [start, end) pairs."""
+    total = float(sum(weights))
+    bounds, i, acc, n = [], 0, 0.0, len(weights)
+    for j in range(n_blocks):
+        target = total * (j + 1) / n_blocks
+        start = i
+        while i < n and n - i > n_blocks - j - 1:
+            w = weights[i]
+            if i > start and (acc >= target or (acc + w / 2.0 > target and j < n_blocks - 1)):
+                break
+            acc += w
+            i += 1
+        bounds.append((start, i))
+    if i < n:  # the last block takes whatever is left
+        bounds[-1] = (bounds[-1][0], n)
+    return bounds
+
+
+def partition(n_layer: int, n_stages: int, cfg: Optional[GPT2Config] = None):
+    """Contiguous layer ranges [a, b) per stage.
+
+    Without `cfg`: an equal split of the layer chain.  With `cfg`: OP-Fence's
+    FLOP-proportional split (opfence.py:412-424) of the operator chain
+    [embeddings, block 0 .. block n-1, LM head]: the head weighs several blocks
+    (GPT-2 medium: 3.5), so the last stage gets fewer blocks.
+    """
+    if cfg is None:
+        bounds = [round(i * n_layer / n_stages) for i in range(n_stages + 1)]
+        return [(bounds[i], bounds[i + 1]) for i in range(n_stages)]
+    blk, head = op_flops(cfg)
+    weights = [1.0] + [blk] * n_layer + [head]  # item 0: embeddings (negligible FLOPs)
+    out = []
+    for a, b in proportional_split(weights, n_stages):
+        # item i >= 1 is block i - 1; the embeddings and the head stay with stages 0 / S-1
+        out.append((max(a - 1, 0) if a > 0 else 0, min(max(b - 1, 0), n_layer)))
+    out[0] = (0, out[0][1])
+    out[-1] = (out[-1][0], n_layer)
+    return out
 
 
 def make_stage(cfg: GPT2Config, s: int, n_stages: int, device, seed: int = 0, sdpa: bool = True) -> Stage:
-    a, b = partition(cfg.n_layer, n_stages)[s]
+    a, b = partition(cfg.n_layer, n_stages, cfg)[s]
     return Stage(cfg, a, b, s == 0, s == n_stages - 1, sdpa, seed).to(device)
 
 
@@ -475,7 +527,8 @@ def run_pipeline(model: str = "medium", plan_mode: str = "uniform", ratio: float
                                   "adatopk": "two-cluster alpha-beta model"}.get(plan_mode),
             "fp_model": model,
             "schedule": "GPipe fill-drain (executor.py:389-404), bf16 autocast, fp32 boundaries",
-            "partition": "contiguous equal layers (OP-Fence split of a homogeneous chain)",
+            "partition": "OP-Fence FLOP-proportional contiguous split of [embeddings, blocks, head]: "
+                         + str(partition(cfg.n_layer, world, cfg)),
             "data": "synthetic tokens, random init"}
 
 
@@ -537,7 +590,7 @@ def synthetic_batch(cfg: GPT2Config, batch: int, seq_len: int, device, seed: int
     return tok[:, :-1].contiguous(), tok[:, 1:].contiguous()
 
 
-__all__ = ["GPT2Config", "GPT2_SMALL", "GPT2_MEDIUM", "GPT2_XL", "GPT2_TINY", "partition", "make_stage",
+__all__ = ["GPT2Config", "GPT2_SMALL", "GPT2_MEDIUM", "GPT2_XL", "GPT2_TINY", "partition", "proportional_split", "op_flops", "make_stage",
            "link_plan", "two_cluster_link_times", "measure_link_times", "measured_link_plan", "eq3_pipeline_time",
            "eq7_pipeline_time", "des_chain_fp_time", "VirtualPipeline", "DistPipeline", "synthetic_batch", "run_pipeline",
            ]

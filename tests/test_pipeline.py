@@ -248,3 +248,35 @@ def test_des_chain_matches_reference_simulator():
                                                               for s in range(S)}}
         tr = simulate(dag, sched, costs, net, n_b=n_b)
         assert PL.des_chain_fp_time(C, M, n_b) == tr.makespan_fp, (trial, S, n_b)
+
+
+def test_proportional_split_matches_opfence():
+    """proportional_split restates OP-Fence's greedy split (opfence.py:285-315)
+    for equal shares; checked on hand cases and, when the reference is
+    importable, against its _proportional_split on random weight chains."""
+    import random
+
+    assert PL.proportional_split([1.0] * 8, 4) == [(0, 2), (2, 4), (4, 6), (6, 8)]
+    assert PL.proportional_split([1.0, 1.0, 1.0, 5.0], 2) == [(0, 3), (3, 4)]
+    med = PL.partition(24, 4, PL.GPT2_MEDIUM)
+    assert med[0][0] == 0 and med[-1][1] == 24 and all(a <= b for a, b in med)
+    assert med[-1][1] - med[-1][0] < med[0][1] - med[0][0]  # the head's stage holds fewer blocks
+    ref = "/root/reference/pkg/src"
+    if not os.path.isdir(ref):
+        pytest.skip("reference not mounted")
+    import sys
+    sys.path.insert(0, ref)
+    try:
+        from geopipe.opfence import _proportional_split
+    finally:
+        sys.path.remove(ref)
+    rng = random.Random(11)
+    for _ in range(300):
+        n, S = rng.randint(1, 40), rng.randint(1, 9)
+        w = [rng.choice([1.0, rng.uniform(0.1, 10.0), rng.uniform(10.0, 100.0)]) for _ in range(n)]
+        blocks = _proportional_split(list(range(n)), w, [1.0] * S)
+        want = []
+        for b in blocks:
+            start = b[0] if b else (want[-1][1] if want else 0)
+            want.append((start, start + len(b)))
+        assert PL.proportional_split(w, S) == want, (w, S)
