@@ -555,3 +555,40 @@ def test_decompress_sortedness_flag_is_exact(cuda, layout):
     missed = [c for c, f in zip(cases, flags[1:]) if not f & _lib.FLAG_UNSORTED]
     assert not missed, missed[:10]
     np.testing.assert_array_equal(idx.cpu().numpy(), h)
+
+
+@pytest.mark.parametrize("dtype", [torch.float32, torch.bfloat16])
+def test_maximum_vector_length(cuda, dtype):
+    """d = 2^31 - 1 (8.6 GB of fp32, the kernels' index width) compresses and
+    round-trips, checked by size-independent properties: k strictly increasing
+    indices, every kept |x| >= every dropped |x| with magnitude ties resolved to
+    the lowest indices, decompress = x on the support and 0 elsewhere.
+    d = 2^31 is rejected with an argument error rather than truncated.  fp32
+    and bf16 (selection on the exact fp32 upcast)."""
+    n = 1 << 31
+    g = torch.Generator(device=cuda).manual_seed(31)
+    buf = torch.empty(n, device=cuda, dtype=dtype)
+    buf.normal_(generator=g)  # bf16: ~32K distinct magnitudes, so the tie rule decides most of the selection
+    x = buf[: n - 1]
+    d, ratio = x.numel(), 1e4
+    p = P.topk_compress(x, ratio)
+    k = P.select_k(d, ratio)
+    idx = p.indices
+    assert idx.numel() == k and bool((idx[1:] > idx[:-1]).all()) and int(idx[0]) >= 0 and int(idx[-1]) < d
+    kept = x[idx].float().abs()
+    thr = float(kept.min())
+    a = x.float().abs()
+    a[idx] = -1.0
+    assert float(a.max()) <= thr
+    tied_dropped = torch.nonzero(a == thr).flatten()
+    if tied_dropped.numel():
+        assert int(idx[kept == thr].max()) < int(tied_dropped.min())
+    del a, tied_dropped
+    out = P.topk_decompress(p)
+    assert torch.equal(out[idx], x[idx])
+    out[idx] = 0.0
+    assert int(torch.count_nonzero(out)) == 0
+    del out, p
+    torch.cuda.empty_cache()
+    with pytest.raises(ValueError):
+        P.topk_compress(buf, ratio)
