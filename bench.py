@@ -331,6 +331,11 @@ def run_ours(args, rank, world, local_rank):
         for s_ in extra_streams:
             cur.wait_stream(s_)
 
+    # diagnostic only: skip the frame copies (the receive buffers keep the
+    # identical frames of earlier steps), isolating the handoff's own cost
+    nocopy_env = os.environ.get("GP_BENCH_NOCOPY") == "1"
+    nocopy = False  # switched on after both receive-buffer parities hold real frames
+
     def compress_all(ev=None, parity=0):
         def body(i, u, st):
             if ev is not None:
@@ -342,7 +347,7 @@ def run_ours(args, rank, world, local_rank):
                 done[i].record(st)
         done = [torch.cuda.Event() for _ in units] if peer and not direct and not pull else None
         on_streams(body)
-        if peer and not direct and not pull:
+        if peer and not direct and not pull and not nocopy:
             # copies in the estimated order the frames complete, round-robin over the copy streams
             for n_, i in enumerate(copy_order):
                 u = units[i]
@@ -392,6 +397,11 @@ def run_ours(args, rank, world, local_rank):
     # decompress launches; the NCCL frame exchange runs eagerly in between at
     # N>1): launch-bound sequences of 24 kernels are what graphs are for.
     graphs = None
+    if nocopy_env:
+        step()
+        step()
+        torch.cuda.synchronize(dev)
+        nocopy = True
     if not args.no_graph:
         step()  # first launches (kernel attributes are set outside any capture)
         torch.cuda.synchronize(dev)
