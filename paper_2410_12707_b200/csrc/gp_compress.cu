@@ -60,6 +60,9 @@ namespace gp {
 constexpr int kMaxGridSpec = 160;      // largest grid: the one-round-trip FC gather stages G*32 keys in smem
 constexpr uint32_t kRing = 4;          // 1 KiB rows in flight per warp (two 2-row bulk copies into smem)
 constexpr uint32_t kFcCapBig = 65536;  // final candidates the fast path accepts in total
+#ifndef GP_DEFER_REST
+#define GP_DEFER_REST 1
+#endif
 #ifndef GP_PREFETCH_ROWS
 #define GP_PREFETCH_ROWS 8
 #endif
@@ -377,8 +380,8 @@ __global__ void __launch_bounds__(kCompressThreads, 1) compress_kernel(const Com
 
   // ---- the unit's rows (1 KiB each) stream through a per-warp ring of two
   // 2 KiB slots, each holding a row pair filled by one bulk (TMA) copy that
-  // completes on the slot's mbarrier; the first two pairs are requested before
-  // anything else
+  // completes on the slot's mbarrier; row pair 0 (the watermark's sample) is
+  // requested before anything else, the rest once it has arrived
   const uint32_t nch = a.aligned ? n / EPL : 0u;  // full 32-byte chunks in the unit
   const uint32_t nrow = (nch + 31) / 32;
   const uint32_t npair = (nrow + 1) / 2;
@@ -393,13 +396,18 @@ __global__ void __launch_bounds__(kCompressThreads, 1) compress_kernel(const Com
     bulk_load_async(ring + slot * 2048u, xw + (size_t)p * 512u, min(64u, nch - p * 64u) * 32u, mbar + slot * 8u,
                     policy);
   };
+  // the rest of the warp's opening requests: the other ring pairs and, for a
+  // short unit, its remaining rows sent to L2 (no second HBM round trip)
+  auto issue_rest = [&]() {
+    for (uint32_t p = 1; p < min(npair, kPairs); ++p) issue(p, p);
+    if (nrow > kRing && nrow <= kRing + kPrefetchRows)
+      prefetch_l2_bulk(xw + (size_t)kRing * 256u, (nch - kRing * 32u) * 32u);
+  };
   if (lane == 0) {
     for (uint32_t s = 0; s < kPairs; ++s) mbar_init(mbar + s * 8u, 1u);
     fence_mbar_init();
-    for (uint32_t p = 0; p < min(npair, kPairs); ++p) issue(p, p);
-    // a short unit sends its remaining rows to L2 now (no second HBM round trip)
-    if (nrow > kRing && nrow <= kRing + kPrefetchRows)
-      prefetch_l2_bulk(xw + (size_t)kRing * 256u, (nch - kRing * 32u) * 32u);
+    if (npair > 0) issue(0, 0);
+    if (!GP_DEFER_REST) issue_rest();
   }
   __syncwarp();
 
@@ -410,6 +418,10 @@ __global__ void __launch_bounds__(kCompressThreads, 1) compress_kernel(const Com
   __syncthreads();
   if (nrow > 0) {
     mbar_wait(mbar, 0u);  // row pair 0
+    // deferred: the watermark needs only row pair 0 of every warp, so the
+    // rest of the unit is requested once this warp's pair 0 is in (it then
+    // streams in under the watermark's barriers instead of ahead of row 0s)
+    if (GP_DEFER_REST && lane == 0) issue_rest();
     uint32_t ns = 0, mb = 0;
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
