@@ -54,6 +54,14 @@ class SparsePayload:
     indices: torch.Tensor
     original_len: int
     frame: Optional[torch.Tensor] = field(default=None, repr=False, compare=False)
+    # set by topk_compress: (indices tensor, its _version, original_len) when
+    # the kernel wrote this payload.  While `indices` is that same tensor, at
+    # that version, with that length, the indices are known to be strictly
+    # increasing and in range, so topk_decompress need not read its validation
+    # flag back (no host sync); replacing the indices, any in-place write to
+    # them (or their frame: views share the version counter) or a new
+    # original_len restores the synchronous check.
+    _produced: Optional[tuple] = field(default=None, repr=False, compare=False)
 
     @property
     def k(self) -> int:
@@ -220,7 +228,7 @@ def topk_compress(vector, ratio: float, *, stream=None) -> SparsePayload:
         flat.data_ptr(), code, d, k, idx.data_ptr(), 8, fvals.data_ptr(), _lib.DTYPE_F32,
         None if code == _lib.DTYPE_F32 else values.data_ptr(), frame.data_ptr(), ws_ptr, ws_bytes, sp)
     raise_for_status(st, "gp_topk_compress", ratio)
-    return SparsePayload(values=values, indices=idx, original_len=d, frame=frame)
+    return SparsePayload(values=values, indices=idx, original_len=d, frame=frame, _produced=(idx, idx._version, d))
 
 
 def topk_decompress(payload: SparsePayload, *, out: Optional[torch.Tensor] = None, accumulate: bool = False,
@@ -231,7 +239,9 @@ def topk_decompress(payload: SparsePayload, *, out: Optional[torch.Tensor] = Non
     reference).  With `check=True` (default, reference behaviour) the device
     validation flag is read back and IndexOutOfRange is raised synchronously;
     unsorted or repeated indices are re-run through the general scatter with
-    numpy's last-write-wins semantics.
+    numpy's last-write-wins semantics.  A payload made by topk_compress and not
+    modified since is valid by construction, so its flag is not read back (no
+    host sync); any other payload is checked.
     """
     values, indices = payload.values, payload.indices
     device = _device(values.device if isinstance(values, torch.Tensor) and values.is_cuda else None)
@@ -261,6 +271,10 @@ def topk_decompress(payload: SparsePayload, *, out: Optional[torch.Tensor] = Non
     st = L.gp_topk_decompress(indices.data_ptr(), ib, values.data_ptr(), code, k, d, out.data_ptr(), out_code,
                               1 if accumulate else 0, err.data_ptr(), sp)
     raise_for_status(st, "gp_topk_decompress", indices)
+    produced = getattr(payload, "_produced", None)
+    if check and produced is not None and payload.indices is produced[0] and \
+            produced[1:] == (payload.indices._version, int(payload.original_len)):
+        check = False  # a kernel-made, unmodified payload: the flag cannot be raised
     if check:
         flag = int(err.item())
         if flag & _lib.FLAG_UNSORTED and not accumulate:

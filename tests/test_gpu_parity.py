@@ -592,3 +592,29 @@ def test_maximum_vector_length(cuda, dtype):
     torch.cuda.empty_cache()
     with pytest.raises(ValueError):
         P.topk_compress(buf, ratio)
+
+
+def test_decompress_skips_sync_only_for_unmodified_payloads(cuda):
+    """A payload made by topk_compress decompresses without reading the
+    validation flag back; replacing or modifying its indices (or its length)
+    restores the reference's synchronous IndexOutOfRange check."""
+    import dataclasses
+
+    x = torch.randn(100_000, device=cuda)
+    p = P.topk_compress(x, 10)
+    ref = torch.zeros_like(x)
+    ref[p.indices] = x[p.indices]
+    assert torch.equal(P.topk_decompress(p), ref)
+    q = P.topk_compress(x, 10)
+    q.indices[0] = -1  # in place (a view of the frame): the version changes
+    with pytest.raises(P.IndexOutOfRange):
+        P.topk_decompress(q)
+    r = P.topk_compress(x, 10)
+    bad = r.indices.clone()
+    bad[-1] = 10 ** 6
+    with pytest.raises(P.IndexOutOfRange):
+        P.topk_decompress(dataclasses.replace(r, indices=bad))
+    s = P.topk_compress(x, 10)
+    s.original_len = 50_000
+    with pytest.raises(P.IndexOutOfRange):
+        P.topk_decompress(s)
