@@ -10,8 +10,9 @@
 // then the range is produced as 32 KiB tiles built in shared memory (zeros, or
 // for mode 1 — residual add, not in the reference — the current contents),
 // the tile's entries are streamed in coalesced batches and scattered into smem,
-// and the tile is written to HBM once with 128-bit stores: no output line is
-// touched twice (a zero-then-scatter in global memory re-reads every line a
+// and the tile is written to HBM once by a bulk (TMA) shared->global store
+// issued by one thread (three tile buffers rotate so none is refilled before
+// its store has read it): no output line is touched twice (a zero-then-scatter in global memory re-reads every line a
 // value lands in once the output exceeds L2).  The same launch validates the
 // index array: each CTA
 // checks a 1/grid share of the k-1 adjacent pairs (strictly increasing) and
@@ -30,7 +31,13 @@ namespace gp {
 
 constexpr int kDecThreads = 512;
 constexpr int kDecBlocksPerSm = 4;
-constexpr int kTileBytes = 16 * 1024;   // smem output tile (double-buffered)
+constexpr int kTileBytes = 16 * 1024;   // smem output tile
+#ifndef GP_DEC_TMA
+#define GP_DEC_TMA 1
+#endif
+// full tiles leave shared memory by one bulk (TMA) store: three buffers, so a
+// buffer is refilled only after its store has read it (no extra barrier)
+constexpr int kTileBufs = GP_DEC_TMA ? 3 : 2;
 constexpr int64_t kMinChunk = 8192;
 #ifndef GP_SPARSE_DENSITY_INV
 #define GP_SPARSE_DENSITY_INV 20
@@ -152,7 +159,8 @@ __global__ void __launch_bounds__(kDecThreads, kDecBlocksPerSm) decompress_kerne
     }                                                            \
   } while (0)
   DSTAMP(0);
-  __shared__ __align__(16) OT tiles[2][kTileElems];
+  extern __shared__ __align__(128) unsigned char dec_smem[];  // kTileBufs tiles
+  OT(*tiles)[kTileElems] = reinterpret_cast<OT(*)[kTileElems]>(dec_smem);
   __shared__ int64_t sh_lo;
   const uint32_t tid = threadIdx.x, lane = tid & 31;
   const int64_t o0 = min((int64_t)blockIdx.x * chunk, d);
@@ -232,7 +240,7 @@ __global__ void __launch_bounds__(kDecThreads, kDecBlocksPerSm) decompress_kerne
   // Output tiles are built in shared memory (zeros or, mode 1, the current
   // contents), the tile's entries are scattered into smem, and the tile is
   // written once with 128-bit stores: every output line reaches HBM once.
-  for (int64_t t0 = o0; t0 < o1; t0 += kTileElems, par ^= 1) {
+  for (int64_t t0 = o0; t0 < o1; t0 += kTileElems, par = par + 1 == kTileBufs ? 0 : par + 1) {
     OT* tile = tiles[par];
     const int n = (int)min((int64_t)kTileElems, o1 - t0);
     const bool full = vec_ok && n == kTileElems;
@@ -266,12 +274,26 @@ __global__ void __launch_bounds__(kDecThreads, kDecBlocksPerSm) decompress_kerne
       nhave = fetch(base + kDecThreads, ni, nv);
     }
     if (full) {
-      uint4* ov = reinterpret_cast<uint4*>(out + t0);
-      for (int i = tid; i < kVecs; i += kDecThreads) ov[i] = tv[i];
+      if (GP_DEC_TMA) {
+        // the tile is complete (the loop left after a barrier): one thread
+        // hands it to the bulk-copy engine; waiting until at most this group
+        // is still reading keeps every buffer's refill, two tiles on, behind
+        // a barrier that follows the wait
+        if (tid == 0) {
+          fence_proxy_async_smem();
+          bulk_store_async(out + t0, smem_addr(tile), (uint32_t)kTileBytes);
+          bulk_commit();
+          bulk_wait_read<1>();
+        }
+      } else {
+        uint4* ov = reinterpret_cast<uint4*>(out + t0);
+        for (int i = tid; i < kVecs; i += kDecThreads) ov[i] = tv[i];
+      }
     } else {
       for (int i = tid; i < n; i += kDecThreads) out[t0 + i] = tile[i];
     }
   }
+  if (GP_DEC_TMA && tid == 0) bulk_wait_all();  // the stores must finish before the CTA's smem goes away
   DSTAMP(3);
   if (pair_check_rest(idx, pb + tid + kDecThreads, pe)) bad = true;
   if (__syncthreads_or(bad) && tid == 0) atomicOr(err, 2u);
@@ -395,7 +417,9 @@ static int run_fast(const DecompressArgs& a, const DeviceInfo& dev, cudaStream_t
   if (dev.ordinal < 0 || dev.ordinal >= kMaxDevices) return 5;
   if (!carveout_set[dev.ordinal].load(std::memory_order_acquire)) {
     if (cudaFuncSetAttribute(decompress_kernel<IT, VT, OT>, cudaFuncAttributePreferredSharedMemoryCarveout,
-                             cudaSharedmemCarveoutMaxShared) != cudaSuccess)
+                             cudaSharedmemCarveoutMaxShared) != cudaSuccess ||
+        cudaFuncSetAttribute(decompress_kernel<IT, VT, OT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             kTileBufs * kTileBytes) != cudaSuccess)
       return 5;
     carveout_set[dev.ordinal].store(true, std::memory_order_release);
   }
@@ -403,7 +427,7 @@ static int run_fast(const DecompressArgs& a, const DeviceInfo& dev, cudaStream_t
     decompress_sparse_kernel<IT, VT, OT><<<(unsigned)grid, kDecThreads, 0, s>>>(
         (const IT*)a.idx, (const VT*)a.vals, a.k, a.d, chunk, (OT*)a.out, a.err);
   } else {
-    decompress_kernel<IT, VT, OT><<<(unsigned)grid, kDecThreads, 0, s>>>(
+    decompress_kernel<IT, VT, OT><<<(unsigned)grid, kDecThreads, kTileBufs * kTileBytes, s>>>(
         (const IT*)a.idx, (const VT*)a.vals, a.k, a.d, chunk, (OT*)a.out, a.mode, a.err, a.dbg);
   }
   return cudaGetLastError() == cudaSuccess ? 0 : 5;
@@ -456,7 +480,8 @@ int debug_decompress_occupancy() {
   int nb = -1;
   cudaFuncSetAttribute(decompress_kernel<int64_t, float, float>, cudaFuncAttributePreferredSharedMemoryCarveout,
                        cudaSharedmemCarveoutMaxShared);
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, decompress_kernel<int64_t, float, float>, kDecThreads, 0);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, decompress_kernel<int64_t, float, float>, kDecThreads,
+                                                kTileBufs * kTileBytes);
   cudaFuncAttributes fa;
   cudaFuncGetAttributes(&fa, decompress_kernel<int64_t, float, float>);
   return nb * 1000000 + fa.numRegs * 1000 + (int)(fa.sharedSizeBytes / 1024);
