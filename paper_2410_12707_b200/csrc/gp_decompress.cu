@@ -4,20 +4,22 @@
 //     if k and (indices.min() < 0 or indices.max() >= d): raise IndexOutOfRange
 //     out = np.zeros(d, values.dtype); out[indices] = values
 //
-// Fast path (indices strictly increasing, as topk_compress emits them): two
-// CTAs per SM, each owning one contiguous output range.  Warps 0/1 locate the
-// range's slice of the index array with an interpolation-guided 32-ary search;
-// then the range is produced as 32 KiB tiles built in shared memory (zeros, or
-// for mode 1 — residual add, not in the reference — the current contents),
-// the tile's entries are streamed in coalesced batches and scattered into smem,
-// and the tile is written to HBM once by a bulk (TMA) shared->global store
-// issued by one thread (three tile buffers rotate so none is refilled before
-// its store has read it): no output line is touched twice (a zero-then-scatter in global memory re-reads every line a
-// value lands in once the output exceeds L2).  The same launch validates the
-// index array: each CTA
-// checks a 1/grid share of the k-1 adjacent pairs (strictly increasing) and
-// CTA 0 checks idx[0] >= 0 and idx[k-1] < d; violations are reported in an
-// asynchronous device flag (GP_FLAG_*).
+// Fast path (indices strictly increasing, as topk_compress emits them): four
+// 512-thread CTAs per SM, each owning one contiguous output range.  One round
+// of 512 probes around the interpolation guess k*o0/d brackets the range's
+// first entry (a 32-ary warp search when the probes miss); then the range is
+// produced as 16 KiB tiles built in shared memory (zeros, or for mode 1 --
+// residual add, not in the reference -- the current contents), the tile's
+// entries are streamed in coalesced batches and scattered into smem, and each
+// full tile is written to HBM once by a bulk (TMA) shared->global store issued
+// by one thread (three tile buffers rotate, so none is refilled before its
+// store has read it).  No output line is touched twice: a zero-then-scatter in
+// global memory re-reads every line a value lands in once the output exceeds
+// L2.  Sparse payloads that fit in L2 take a fill+scatter kernel instead.  The
+// same launch validates the index array: each CTA checks a 1/grid share of the
+// k-1 adjacent pairs (strictly increasing) and CTA 0 checks idx[0] >= 0 and
+// idx[k-1] < d; violations are reported in an asynchronous device flag
+// (GP_FLAG_*).
 //
 // General path (unsorted / repeated indices) reproduces numpy's
 // last-write-wins `out[indices] = values` with an atomicMax "winner" pass.
