@@ -285,3 +285,25 @@ def test_proportional_split_matches_opfence():
             start = b[0] if b else (want[-1][1] if want else 0)
             want.append((start, start + len(b)))
         assert PL.proportional_split(w, S) == want, (w, S)
+
+
+@pytest.mark.parametrize("cfg", [PL.GPT2_SMALL, PL.GPT2_MEDIUM, PL.GPT2_XL], ids=["small", "medium", "xl"])
+def test_flop_partition_covers_layers_and_every_stage_has_parameters(cfg):
+    """The OP-Fence split at 1..8 stages tiles [0, n_layer) contiguously, and
+    every stage owns parameters (embeddings, blocks or the head), so each rank
+    of the N=8 bench has something to optimise; the head-only last stage (GPT-2
+    medium at 8 stages) runs forward and backward."""
+    for S in range(1, 9):
+        parts = PL.partition(cfg.n_layer, S, cfg)
+        assert len(parts) == S and parts[0][0] == 0 and parts[-1][1] == cfg.n_layer
+        assert all(parts[i][1] == parts[i + 1][0] for i in range(S - 1))
+        for s, (a, b) in enumerate(parts):
+            assert a <= b and (b > a or s in (0, S - 1)), (S, parts)
+    a, b = PL.partition(PL.GPT2_MEDIUM.n_layer, 8, PL.GPT2_MEDIUM)[-1]
+    assert a == b == 24  # the head alone
+    tiny_head = PL.Stage(PL.GPT2_TINY, 4, 4, first=False, last=True)
+    x = torch.randn(2, 16, PL.GPT2_TINY.n_embd, requires_grad=True)
+    tgt = torch.randint(0, PL.GPT2_TINY.vocab, (2, 16))
+    loss = tiny_head(x, tgt)
+    loss.backward()
+    assert torch.isfinite(loss) and x.grad is not None and sum(p.numel() for p in tiny_head.parameters()) > 0
