@@ -618,3 +618,41 @@ def test_decompress_skips_sync_only_for_unmodified_payloads(cuda):
     s.original_len = 50_000
     with pytest.raises(P.IndexOutOfRange):
         P.topk_decompress(s)
+
+
+@pytest.mark.parametrize("dtype", [torch.bfloat16, torch.float64])
+def test_decompress_accumulate_bf16_f64(cuda, dtype):
+    """Residual mode (tiled kernel) in bf16 and f64: out[idx] += vals, rounded
+    like torch (bf16: fp32 add, round to nearest even), bit for bit."""
+    g = torch.Generator(device=cuda).manual_seed(21)
+    x = torch.randn(3_000_000, device=cuda, generator=g).to(dtype)
+    base = torch.randn(3_000_000, device=cuda, generator=g).to(dtype)
+    p = P.topk_compress(x, 50)
+    out = base.clone()
+    P.topk_decompress(p, out=out, accumulate=True)
+    ref = base.clone()
+    ref[p.indices] += x[p.indices]
+    assert torch.equal(out.view(torch.int16 if dtype == torch.bfloat16 else torch.int64),
+                       ref.view(torch.int16 if dtype == torch.bfloat16 else torch.int64))
+
+
+@pytest.mark.parametrize("ratio", [10, 100])
+def test_decompress_frame_misaligned_output(cuda, ratio):
+    """An output pointer that is not 16-byte aligned takes the element-wise store
+    path (bulk TMA stores need 16-byte alignment); the result is still exact."""
+    L = _lib.lib()
+    g = torch.Generator(device=cuda).manual_seed(ratio)
+    x = torch.randn(2_000_000, device=cuda, generator=g)
+    d = x.numel()
+    p = P.topk_compress(x, ratio)
+    k = p.k
+    buf = torch.full((d + 1,), float("nan"), device=cuda)
+    out = buf[1:]  # 4-byte offset
+    assert out.data_ptr() % 16 != 0
+    err = torch.zeros(1, dtype=torch.int32, device=cuda)
+    s = torch.cuda.current_stream().cuda_stream
+    assert L.gp_topk_decompress_frame(p.frame.data_ptr(), k, d, out.data_ptr(), 0, 0, err.data_ptr(), s) == 0
+    assert int(err.item()) == 0
+    ref = torch.zeros_like(x)
+    ref[p.indices] = x[p.indices]
+    assert torch.equal(out, ref) and bool(torch.isnan(buf[0]))
