@@ -210,6 +210,11 @@ def topk_compress(vector, ratio: float, *, stream=None) -> SparsePayload:
     the f32 wire values.  Runs the cooperative sm_100a select+compact kernel.
     """
     device = _device(vector.device if isinstance(vector, torch.Tensor) and vector.is_cuda else None)
+    with torch.cuda.device(device):  # launches go to the tensor's GPU whatever the current device
+        return _topk_compress_on(vector, ratio, device, stream)
+
+
+def _topk_compress_on(vector, ratio: float, device: torch.device, stream) -> SparsePayload:
     flat = _as_device_flat(vector, device)
     d = flat.numel()
     if d == 0:
@@ -243,8 +248,14 @@ def topk_decompress(payload: SparsePayload, *, out: Optional[torch.Tensor] = Non
     modified since is valid by construction, so its flag is not read back (no
     host sync); any other payload is checked.
     """
-    values, indices = payload.values, payload.indices
+    values = payload.values
     device = _device(values.device if isinstance(values, torch.Tensor) and values.is_cuda else None)
+    with torch.cuda.device(device):  # launches go to the payload's GPU whatever the current device
+        return _topk_decompress_on(payload, device, out, accumulate, check, stream)
+
+
+def _topk_decompress_on(payload, device: torch.device, out, accumulate: bool, check: bool, stream) -> torch.Tensor:
+    values, indices = payload.values, payload.indices
     if not isinstance(values, torch.Tensor) or not values.is_cuda:
         values = torch.as_tensor(np.asarray(values)).to(device)
     if not isinstance(indices, torch.Tensor) or not indices.is_cuda:

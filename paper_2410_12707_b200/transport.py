@@ -63,6 +63,10 @@ class FrameCodec:
         self.err = torch.zeros(1, dtype=torch.int32, device=self.device)
 
     def compress(self, x: torch.Tensor, ratio: float, frame: Optional[torch.Tensor] = None) -> torch.Tensor:
+        with torch.cuda.device(self.device):
+            return self._compress(x, ratio, frame)
+
+    def _compress(self, x: torch.Tensor, ratio: float, frame: Optional[torch.Tensor]) -> torch.Tensor:
         flat = x.reshape(-1)
         if not flat.is_contiguous():
             flat = flat.contiguous()
@@ -78,6 +82,10 @@ class FrameCodec:
         return frame
 
     def decompress(self, frame: torch.Tensor, out: torch.Tensor, ratio: float, accumulate: bool = False):
+        with torch.cuda.device(self.device):
+            return self._decompress(frame, out, ratio, accumulate)
+
+    def _decompress(self, frame: torch.Tensor, out: torch.Tensor, ratio: float, accumulate: bool):
         d = out.numel()
         k = select_k(d, ratio)
         st = _lib.lib().gp_topk_decompress_frame(frame.data_ptr(), k, d, out.data_ptr(), _DTYPE_CODE[out.dtype],

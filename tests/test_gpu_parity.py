@@ -656,3 +656,20 @@ def test_decompress_frame_misaligned_output(cuda, ratio):
     ref = torch.zeros_like(x)
     ref[p.indices] = x[p.indices]
     assert torch.equal(out, ref) and bool(torch.isnan(buf[0]))
+
+
+def test_tensor_on_another_device_than_current(cuda):
+    """A tensor on cuda:1 while cuda:0 is current: the drop-in launches on the
+    tensor's GPU and the frame equals the one produced on cuda:0."""
+    if torch.cuda.device_count() < 2:
+        pytest.skip("needs 2 GPUs (run under gpurun --gpus 2)")
+    g = torch.Generator(device=cuda).manual_seed(5)
+    x0 = torch.randn(1_500_000, device=cuda, generator=g)
+    x1 = x0.to("cuda:1")
+    with torch.cuda.device(0):
+        p1 = P.topk_compress(x1, 100)
+        d1 = P.topk_decompress(p1)
+    p0 = P.topk_compress(x0, 100)
+    assert p1.indices.device.index == 1 and d1.device.index == 1
+    assert p1.to_bytes() == p0.to_bytes()
+    assert torch.equal(d1.cpu(), P.topk_decompress(p0).cpu())
