@@ -34,6 +34,9 @@ namespace gp {
 constexpr int kDecThreads = 512;
 constexpr int kDecBlocksPerSm = 4;
 constexpr int kTileBytes = 16 * 1024;   // smem output tile
+#ifndef GP_DEC_EVICT_FIRST
+#define GP_DEC_EVICT_FIRST 1
+#endif
 #ifndef GP_DEC_TMA
 #define GP_DEC_TMA 1
 #endif
@@ -283,7 +286,10 @@ __global__ void __launch_bounds__(kDecThreads, kDecBlocksPerSm) decompress_kerne
         // a barrier that follows the wait
         if (tid == 0) {
           fence_proxy_async_smem();
-          bulk_store_async(out + t0, smem_addr(tile), (uint32_t)kTileBytes);
+          if (GP_DEC_EVICT_FIRST)  // output lines leave L2 first: the frame stays for the pair checks
+            bulk_store_async_hint(out + t0, smem_addr(tile), (uint32_t)kTileBytes, l2_evict_first_policy());
+          else
+            bulk_store_async(out + t0, smem_addr(tile), (uint32_t)kTileBytes);
           bulk_commit();
           bulk_wait_read<1>();
         }
