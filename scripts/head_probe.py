@@ -1,3 +1,4 @@
+"""GPT-2 LM-head cost on B200: bf16 GEMM with N = 50257 vs N padded to 50304, with and without the loss (development aid)."""
 import torch, torch.nn.functional as F, time
 dev = torch.device("cuda")
 B, T, H = 8, 1024, 1024
