@@ -31,9 +31,15 @@
 
 namespace gp {
 
+#ifndef GP_DEC_TILE_KB
+#define GP_DEC_TILE_KB 16
+#endif
+#ifndef GP_DEC_BLOCKS_PER_SM
+#define GP_DEC_BLOCKS_PER_SM 4
+#endif
 constexpr int kDecThreads = 512;
-constexpr int kDecBlocksPerSm = 4;
-constexpr int kTileBytes = 16 * 1024;   // smem output tile
+constexpr int kDecBlocksPerSm = GP_DEC_BLOCKS_PER_SM;
+constexpr int kTileBytes = GP_DEC_TILE_KB * 1024;   // smem output tile
 #ifndef GP_DEC_EVICT_FIRST
 #define GP_DEC_EVICT_FIRST 1
 #endif
