@@ -22,7 +22,7 @@
 //            FSETP) is a candidate; candidates go to the warp's index-ordered
 //            list (shared memory, spilling to the workspace) and into an fb-bit
 //            "fine" histogram (smem window starting at the watermark, flushed by
-//            red.add into one of 2 global replicas).  Sparse steps place
+//            red.add into the global histogram, GP_HIST_COPIES replicas).  Sparse steps place
 //            candidates with ballots; dense steps with one packed warp scan.
 //            -- grid barrier B1 --
 //   stage 2  every CTA sums the replicas from the top and finds the fine bin

@@ -20,7 +20,7 @@ constexpr int kFcCap = 8192;            // final-candidate capacity of the fast 
 
 // control words at the head of the workspace
 #ifndef GP_HIST_COPIES
-#define GP_HIST_COPIES 2
+#define GP_HIST_COPIES 1
 #endif
 constexpr int kHistCopies = GP_HIST_COPIES;  // replicas of the fine histogram (CTA c uses c % copies)
 constexpr int kCtrlBar = 0;             // grid-barrier word (top bit flips per barrier)

@@ -32,7 +32,9 @@ def main(src, md_out, json_out):
     ids = sorted(launches)
     comp = [i for i in ids if names[i].startswith("void compress_kernel")]
     dec = [i for i in ids if "decompress" in names[i]]
-    us = list(units())
+    # bench.py --streams 1 launches the units longest-first by its cost
+    # estimate (bench.py: dense_w 2.2 for r <= 10, 4e6 per unit), stable
+    us = sorted(units(), key=lambda u: -(u[3] * (2.2 if u[2] <= 10 else 1.0) + 4e6))
     lines = ["| unit | kernel | time us | DRAM read MB | DRAM write MB | algorithmic MB | DRAM/alg |",
              "|---|---|---|---|---|---|---|"]
     tot = {"c_t": 0.0, "c_dram": 0.0, "c_alg": 0.0, "d_t": 0.0, "d_dram": 0.0, "d_alg": 0.0}
