@@ -10,7 +10,10 @@ namespace gp {
 
 constexpr int kCompressThreads = 1024;  // 32 warps; block scans assume exactly this
 constexpr int kMaxGrid = 1024;          // max CTAs of the cooperative compress grid
-constexpr int kMinPerCta = 16384;       // elements per CTA below which the grid shrinks
+#ifndef GP_MIN_PER_CTA
+#define GP_MIN_PER_CTA 16384
+#endif
+constexpr int kMinPerCta = GP_MIN_PER_CTA;  // elements per CTA below which the grid shrinks
 constexpr int kCoarseBins = 1 << 12;    // sample histogram (key >> (bits-12))
 constexpr int kFineBitsMax = 20;        // fine candidate histogram: 16..20 bits (grows with d)
 constexpr int kFineBinsMax = 1 << kFineBitsMax;
