@@ -40,6 +40,8 @@ extern "C" {
 /* ---- asynchronous device error flags (decompress) ---------------------- */
 #define GP_FLAG_OUT_OF_RANGE  1u   /* some index < 0 or >= d  (compressor.py:99-100) */
 #define GP_FLAG_UNSORTED      2u   /* indices not strictly increasing (fast path invalid) */
+#define GP_FLAG_HEADER        4u   /* frame header {d,k} disagrees with the receiver's (d, k / k_cap) */
+#define GP_FLAG_BAD_K         8u   /* device-resident k outside [1, min(k_cap, d)] (compress) */
 
 /* Wire frame of the reference (compressor.py:39-44): little-endian
  * {d:u64, k:u64} header, k x i64 indices, k x f32 values. */
@@ -107,10 +109,48 @@ int gp_topk_compress_frame_ctas(const void* x, int dtype, int64_t d, int64_t k,
                                 void* frame_out, void* ws, size_t ws_bytes,
                                 void* stream, int max_ctas);
 
-/* Decompress straight from a reference wire frame on the device. */
+/* Decompress straight from a reference wire frame on the device.  The frame's
+ * {d, k} header is checked against (d, k) in the same launch: a mismatch
+ * raises GP_FLAG_HEADER and nothing is scattered. */
 int gp_topk_decompress_frame(const void* frame, int64_t k, int64_t d,
                              void* out, int out_dtype, int mode,
                              uint32_t* d_err_flag, void* stream);
+
+/* ---- device-resident k (north_star item 4: adaptive bookkeeping kept on the
+ * device).  k is read from device memory at kernel start -- e.g. the k_out of
+ * gp_adatopk_plan -- so re-planning k never round-trips through the host.
+ * Frames are sized for a host-known capacity k_cap (16 + 12*k_cap bytes; the
+ * frame written is 16 + 12*k, values right after the k indices as in the
+ * reference layout).  *k_dev outside [1, min(k_cap, d)] writes nothing but an
+ * invalid header {d, ~0} and raises GP_FLAG_BAD_K; k == d keeps every element
+ * (ratio <= 1, the executor's pass-through, executor.py:210-212).
+ * Replaces topk_compress + to_bytes (compressor.py:79-94, :39-44) with k from
+ * select_k/adatopk_plan evaluated on the device (compressor.py:73-76,111-129). */
+int gp_topk_compress_frame_dk(const void* x, int dtype, int64_t d, const int64_t* k_dev, int64_t k_cap,
+                              void* frame_out, uint32_t* d_err_flag, void* ws, size_t ws_bytes,
+                              void* stream, int max_ctas);
+
+/* Decompress a frame whose k is read from its own header (1 <= k <= k_cap and
+ * header d == d, else GP_FLAG_HEADER and nothing is scattered).  The receive
+ * buffer is sized for k_cap; no size handshake precedes the payload.
+ * Replaces topk_decompress(SparsePayload.from_bytes(raw)), compressor.py:46-53,97-103. */
+int gp_topk_decompress_frame_dk(const void* frame, int64_t d, int64_t k_cap, void* out, int out_dtype, int mode,
+                                uint32_t* d_err_flag, void* stream);
+
+/* Standalone on-device frame pack: {d, k} header, k indices widened to i64,
+ * k values rounded to f32 (IEEE round-to-nearest; exact for f32 / bf16).
+ * Replaces SparsePayload.to_bytes, compressor.py:39-44. */
+int gp_pack_frame(const void* idx, int idx_bytes, const void* vals, int val_dtype, int64_t k, int64_t d,
+                  void* frame_out, void* stream);
+
+/* Standalone on-device frame unpack: k from the frame's header (must be
+ * <= k_cap; d_expect >= 0 also checks the header's d), i64 indices and the
+ * values converted to val_dtype (GP_DTYPE_F64 = the reference's from_bytes,
+ * which returns float64 values).  hdr_out (nullable, device) receives {d, k}.
+ * A bad header raises GP_FLAG_HEADER and unpacks nothing.
+ * Replaces SparsePayload.from_bytes, compressor.py:46-53. */
+int gp_unpack_frame(const void* frame, int64_t k_cap, int64_t d_expect, int64_t* idx_out, void* vals_out,
+                    int val_dtype, int64_t* hdr_out, uint32_t* d_err_flag, void* stream);
 
 /* General scatter for arbitrary (unsorted, possibly repeated) indices with
  * numpy's last-write-wins semantics for `out[indices] = values`.  `scratch`

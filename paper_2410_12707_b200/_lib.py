@@ -17,6 +17,8 @@ DTYPE_BF16 = 1
 DTYPE_F64 = 2
 FLAG_OUT_OF_RANGE = 1
 FLAG_UNSORTED = 2
+FLAG_HEADER = 4   # frame header {d, k} disagrees with the receiver's expectation
+FLAG_BAD_K = 8    # device-resident k outside [1, min(k_cap, d)]
 FRAME_HEADER_BYTES = 16
 
 _SIGS = {
@@ -37,6 +39,13 @@ _SIGS = {
                                    c_void_p, c_void_p]),
     "gp_topk_decompress_frame": (c_int, [c_void_p, c_int64, c_int64, c_void_p, c_int, c_int, c_void_p,
                                          c_void_p]),
+    "gp_topk_compress_frame_dk": (c_int, [c_void_p, c_int, c_int64, c_void_p, c_int64, c_void_p, c_void_p, c_void_p,
+                                          c_size_t, c_void_p, c_int]),
+    "gp_topk_decompress_frame_dk": (c_int, [c_void_p, c_int64, c_int64, c_void_p, c_int, c_int, c_void_p,
+                                            c_void_p]),
+    "gp_pack_frame": (c_int, [c_void_p, c_int, c_void_p, c_int, c_int64, c_int64, c_void_p, c_void_p]),
+    "gp_unpack_frame": (c_int, [c_void_p, c_int64, c_int64, c_void_p, c_void_p, c_int, c_void_p, c_void_p,
+                                c_void_p]),
     "gp_topk_decompress_unsorted": (c_int, [c_void_p, c_int, c_void_p, c_int, c_int64, c_int64, c_void_p, c_int,
                                             c_void_p, c_void_p, c_void_p]),
     "gp_adatopk_plan": (c_int, [POINTER(c_double), c_int, c_double, POINTER(c_int64), POINTER(c_double),

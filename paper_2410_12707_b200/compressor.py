@@ -54,14 +54,16 @@ class SparsePayload:
     indices: torch.Tensor
     original_len: int
     frame: Optional[torch.Tensor] = field(default=None, repr=False, compare=False)
-    # set by topk_compress: (indices tensor, its _version, original_len) when
-    # the kernel wrote this payload.  While `indices` is that same tensor, at
-    # that version, with that length, the indices are known to be strictly
-    # increasing and in range, so topk_decompress need not read its validation
-    # flag back (no host sync); replacing the indices, any in-place write to
-    # them (or their frame: views share the version counter) or a new
-    # original_len restores the synchronous check.
+    # set when the frame was written together with these fields (by the
+    # compress kernel or by from_bytes): (indices, its _version, values, its
+    # _version, original_len).  While all of these still hold, the payload is
+    # unmodified: to_bytes() may return the cached frame, and for kernel-made
+    # payloads topk_decompress need not read its validation flag back (the
+    # indices are strictly increasing and in range by construction).  Any
+    # replaced field (dataclasses.replace included), in-place write (views
+    # share the version counter) or new original_len invalidates it.
     _produced: Optional[tuple] = field(default=None, repr=False, compare=False)
+    _kernel_made: bool = field(default=False, repr=False, compare=False)
 
     @property
     def k(self) -> int:
@@ -76,27 +78,64 @@ class SparsePayload:
         """Wire accounting for the values+indices body (excludes the 16B header)."""
         return self.k * (VALUE_BYTES + INDEX_BYTES)
 
+    def _unmodified(self) -> bool:
+        p = self._produced
+        return (p is not None and self.indices is p[0] and self.indices._version == p[1] and self.values is p[2]
+                and self.values._version == p[3] and int(self.original_len) == p[4])
+
     def to_bytes(self) -> bytes:
-        """Little-endian frame: {d: u64, k: u64}, k x i64 indices, k x f32 values."""
-        if self.frame is not None:
+        """Little-endian frame: {d: u64, k: u64}, k x i64 indices, k x f32 values.
+
+        Always the current fields: the cached device frame when the payload is
+        unmodified, else a frame packed on the device (gp_pack_frame) from the
+        fields as they are now."""
+        if self.frame is not None and self._unmodified():
             return self.frame.cpu().numpy().tobytes()
-        head = struct.pack("<QQ", self.original_len, self.k)
-        idx = np.ascontiguousarray(self.indices.cpu().numpy(), dtype="<i8").tobytes()
-        vals = self.values.cpu()
-        if vals.dtype == torch.bfloat16:
-            vals = vals.float()  # exact widening
-        vals = np.ascontiguousarray(vals.numpy(), dtype="<f4").tobytes()
-        return head + idx + vals
+        values, indices = self.values, self.indices
+        if not (isinstance(values, torch.Tensor) and values.is_cuda):
+            raise TypeError("SparsePayload.values must be a CUDA tensor")
+        device = values.device
+        vals = values.reshape(-1).contiguous()
+        idx = torch.as_tensor(indices, device=device).reshape(-1).contiguous()
+        k = int(vals.numel())
+        if idx.numel() != k:
+            raise ValueError(f"payload has {k} values but {idx.numel()} indices")
+        if idx.dtype not in (torch.int64, torch.int32):
+            idx = idx.to(torch.int64)
+        code = _DTYPE_CODE.get(vals.dtype)
+        if code is None:
+            vals, code = vals.to(torch.float64), _lib.DTYPE_F64  # exact widening of other float/int dtypes
+        frame = torch.empty(16 + 12 * k, dtype=torch.uint8, device=device)
+        with torch.cuda.device(device):
+            st = _lib.lib().gp_pack_frame(idx.data_ptr(), idx.element_size(), vals.data_ptr(), code, k,
+                                          int(self.original_len), frame.data_ptr(), _stream_handle(device))
+        raise_for_status(st, "gp_pack_frame")
+        return frame.cpu().numpy().tobytes()
 
     @classmethod
     def from_bytes(cls, raw: bytes, device=None) -> "SparsePayload":
-        """Parse a frame; like the reference (compressor.py:46-53) values come back as float64."""
+        """Parse a frame; like the reference (compressor.py:46-53) values come back as float64.
+
+        The frame is uploaded once and unpacked on the device (gp_unpack_frame);
+        a buffer shorter than its header's k says raises ValueError, as numpy's
+        `frombuffer(count=k)` does in the reference."""
+        if len(raw) < 16:
+            raise ValueError(f"frame of {len(raw)} bytes has no 16-byte header")
         d, k = struct.unpack_from("<QQ", raw, 0)
+        if len(raw) < 16 + 12 * k:
+            raise ValueError(f"frame of {len(raw)} bytes is shorter than its header's k = {k} entries need")
         dev = _device(device)
         frame = torch.frombuffer(bytearray(raw[: 16 + 12 * k]), dtype=torch.uint8).to(dev)
-        indices = frame[16:16 + 8 * k].view(torch.int64)
-        values = frame[16 + 8 * k:16 + 12 * k].view(torch.float32).to(torch.float64)
-        return cls(values=values, indices=indices, original_len=int(d), frame=frame)
+        indices = torch.empty(k, dtype=torch.int64, device=dev)
+        values = torch.empty(k, dtype=torch.float64, device=dev)
+        err = _Flags.get(dev, _stream_handle(dev))
+        with torch.cuda.device(dev):
+            st = _lib.lib().gp_unpack_frame(frame.data_ptr(), k, d, indices.data_ptr(), values.data_ptr(),
+                                            _lib.DTYPE_F64, None, err.data_ptr(), _stream_handle(dev))
+        raise_for_status(st, "gp_unpack_frame")
+        p = cls(values=values, indices=indices, original_len=int(d), frame=frame)
+        p._produced = (indices, indices._version, values, values._version, int(d))
+        return p
 
 
 @dataclass
@@ -153,12 +192,17 @@ def _device(device=None) -> torch.device:
 
 
 def _stream_handle(device: torch.device, stream=None) -> int:
+    """The raw cudaStream_t of `stream` (None: the current stream of `device`)."""
     s = stream if stream is not None else torch.cuda.current_stream(device)
     return int(s.cuda_stream)
 
 
 class _Workspace:
-    """Per (device, stream) scratch for gp_topk_compress, zeroed once, grown on demand."""
+    """Per (device, stream) scratch for gp_topk_compress, zeroed once, grown on demand.
+
+    A workspace sized for d serves every call with d' <= d (include/adatopk.h),
+    so the cache keeps the largest d it was sized for and replaces the buffer
+    (zeroed anew) only when a longer vector arrives."""
 
     _cache: dict = {}
 
@@ -166,16 +210,42 @@ class _Workspace:
     def get(cls, device: torch.device, stream_ptr: int, d: int, dtype_code: int) -> tuple[int, int]:
         need = int(_lib.lib().gp_topk_workspace_bytes(d, dtype_code))
         key = (device.index, stream_ptr)
-        buf = cls._cache.get(key)
-        if buf is None or buf.numel() < need:
+        ent = cls._cache.get(key)
+        if ent is None or ent[1] < d or ent[0].numel() < need:
+            dd = max(d, ent[1] if ent is not None else 0)
+            need = max(need, int(_lib.lib().gp_topk_workspace_bytes(dd, _lib.DTYPE_F64)))  # any dtype up to dd
             buf = torch.empty(need, dtype=torch.uint8, device=device)
             raise_for_status(_lib.lib().gp_workspace_init(buf.data_ptr(), need, stream_ptr), "gp_workspace_init")
-            cls._cache[key] = buf
-        return buf.data_ptr(), int(buf.numel())
+            ent = (buf, dd)
+            cls._cache[key] = ent
+        return ent[0].data_ptr(), int(ent[0].numel())
 
     @classmethod
     def clear(cls) -> None:
         cls._cache.clear()
+
+
+class _Flags:
+    """Per (device, stream) asynchronous validation flag (one int32), zeroed at
+    creation and re-zeroed only after it was read non-zero: no per-call fill."""
+
+    _cache: dict = {}
+
+    @classmethod
+    def get(cls, device: torch.device, stream_ptr: int) -> torch.Tensor:
+        key = (device.index, stream_ptr)
+        f = cls._cache.get(key)
+        if f is None:
+            f = torch.zeros(1, dtype=torch.int32, device=device)
+            cls._cache[key] = f
+        return f
+
+    @staticmethod
+    def read(flag: torch.Tensor) -> int:
+        v = int(flag.item())
+        if v:
+            flag.zero_()
+        return v
 
 
 def _as_device_flat(vector, device: torch.device) -> torch.Tensor:
@@ -194,12 +264,23 @@ def _as_device_flat(vector, device: torch.device) -> torch.Tensor:
     return t.reshape(-1).contiguous()
 
 
-def _err_flag(device: torch.device) -> torch.Tensor:
-    return torch.zeros(1, dtype=torch.int32, device=device)
-
-
 # ---------------------------------------------------------------------------
 # compress / decompress
+
+
+def _on_stream(stream):
+    """Run the body on `stream` (None: the current stream): staging copies,
+    outputs, the kernels and any flag read are then ordered on that one stream,
+    and the caching allocator records their use there."""
+    return torch.cuda.stream(stream) if stream is not None else _NullCtx()
+
+
+class _NullCtx:
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        return False
 
 
 def topk_compress(vector, ratio: float, *, stream=None) -> SparsePayload:
@@ -210,11 +291,11 @@ def topk_compress(vector, ratio: float, *, stream=None) -> SparsePayload:
     the f32 wire values.  Runs the cooperative sm_100a select+compact kernel.
     """
     device = _device(vector.device if isinstance(vector, torch.Tensor) and vector.is_cuda else None)
-    with torch.cuda.device(device):  # launches go to the tensor's GPU whatever the current device
-        return _topk_compress_on(vector, ratio, device, stream)
+    with torch.cuda.device(device), _on_stream(stream):  # launches go to the tensor's GPU whatever the current device
+        return _topk_compress_on(vector, ratio, device)
 
 
-def _topk_compress_on(vector, ratio: float, device: torch.device, stream) -> SparsePayload:
+def _topk_compress_on(vector, ratio: float, device: torch.device) -> SparsePayload:
     flat = _as_device_flat(vector, device)
     d = flat.numel()
     if d == 0:
@@ -223,7 +304,7 @@ def _topk_compress_on(vector, ratio: float, device: torch.device, stream) -> Spa
     code = _DTYPE_CODE.get(flat.dtype)
     if code is None:
         raise TypeError(f"unsupported dtype {flat.dtype}; expected float32, bfloat16 or float64")
-    sp = _stream_handle(device, stream)
+    sp = _stream_handle(device)
     frame = torch.empty(16 + 12 * k, dtype=torch.uint8, device=device)
     idx = frame[16:16 + 8 * k].view(torch.int64)
     fvals = frame[16 + 8 * k:].view(torch.float32)
@@ -233,7 +314,10 @@ def _topk_compress_on(vector, ratio: float, device: torch.device, stream) -> Spa
         flat.data_ptr(), code, d, k, idx.data_ptr(), 8, fvals.data_ptr(), _lib.DTYPE_F32,
         None if code == _lib.DTYPE_F32 else values.data_ptr(), frame.data_ptr(), ws_ptr, ws_bytes, sp)
     raise_for_status(st, "gp_topk_compress", ratio)
-    return SparsePayload(values=values, indices=idx, original_len=d, frame=frame, _produced=(idx, idx._version, d))
+    p = SparsePayload(values=values, indices=idx, original_len=d, frame=frame)
+    p._produced = (idx, idx._version, values, values._version, d)
+    p._kernel_made = True
+    return p
 
 
 def topk_decompress(payload: SparsePayload, *, out: Optional[torch.Tensor] = None, accumulate: bool = False,
@@ -241,20 +325,21 @@ def topk_decompress(payload: SparsePayload, *, out: Optional[torch.Tensor] = Non
     """Dense length-d vector: kept values at their indices, zero elsewhere (compressor.py:97-103).
 
     `accumulate=True` adds into `out` instead (residual mode; not in the
-    reference).  With `check=True` (default, reference behaviour) the device
-    validation flag is read back and IndexOutOfRange is raised synchronously;
-    unsorted or repeated indices are re-run through the general scatter with
-    numpy's last-write-wins semantics.  A payload made by topk_compress and not
+    reference; its indices must be strictly increasing, else ValueError).
+    With `check=True` (default, reference behaviour) the device validation
+    flag is read back and IndexOutOfRange is raised synchronously; unsorted or
+    repeated indices are re-run through the general scatter with numpy's
+    last-write-wins semantics.  A payload made by topk_compress and not
     modified since is valid by construction, so its flag is not read back (no
     host sync); any other payload is checked.
     """
     values = payload.values
     device = _device(values.device if isinstance(values, torch.Tensor) and values.is_cuda else None)
-    with torch.cuda.device(device):  # launches go to the payload's GPU whatever the current device
-        return _topk_decompress_on(payload, device, out, accumulate, check, stream)
+    with torch.cuda.device(device), _on_stream(stream):  # launches go to the payload's GPU whatever the current device
+        return _topk_decompress_on(payload, device, out, accumulate, check)
 
 
-def _topk_decompress_on(payload, device: torch.device, out, accumulate: bool, check: bool, stream) -> torch.Tensor:
+def _topk_decompress_on(payload, device: torch.device, out, accumulate: bool, check: bool) -> torch.Tensor:
     values, indices = payload.values, payload.indices
     if not isinstance(values, torch.Tensor) or not values.is_cuda:
         values = torch.as_tensor(np.asarray(values)).to(device)
@@ -265,6 +350,8 @@ def _topk_decompress_on(payload, device: torch.device, out, accumulate: bool, ch
     if indices.dtype not in (torch.int64, torch.int32):
         indices = indices.to(torch.int64)
     d, k = int(payload.original_len), int(values.numel())
+    if indices.numel() != k:  # numpy raises on the shape mismatch in the reference (compressor.py:101-102)
+        raise ValueError(f"payload has {k} values but {indices.numel()} indices")
     code = _DTYPE_CODE.get(values.dtype)
     if code is None:
         raise TypeError(f"unsupported value dtype {values.dtype}")
@@ -275,26 +362,25 @@ def _topk_decompress_on(payload, device: torch.device, out, accumulate: bool, ch
     out_code = _DTYPE_CODE[out.dtype]
     if d == 0 and k > 0:
         raise IndexOutOfRange(indices)
-    sp = _stream_handle(device, stream)
-    err = _err_flag(device)
+    sp = _stream_handle(device)
+    err = _Flags.get(device, sp)
     L = _lib.lib()
     ib = indices.element_size()
     st = L.gp_topk_decompress(indices.data_ptr(), ib, values.data_ptr(), code, k, d, out.data_ptr(), out_code,
                               1 if accumulate else 0, err.data_ptr(), sp)
     raise_for_status(st, "gp_topk_decompress", indices)
-    produced = getattr(payload, "_produced", None)
-    if check and produced is not None and payload.indices is produced[0] and \
-            produced[1:] == (payload.indices._version, int(payload.original_len)):
+    if check and getattr(payload, "_kernel_made", False) and payload._unmodified():
         check = False  # a kernel-made, unmodified payload: the flag cannot be raised
     if check:
-        flag = int(err.item())
-        if flag & _lib.FLAG_UNSORTED and not accumulate:
-            err.zero_()
+        flag = _Flags.read(err)
+        if flag & _lib.FLAG_UNSORTED:
+            if accumulate:
+                raise ValueError("residual-mode decompress needs strictly increasing indices")
             scratch = torch.empty(max(d, 1), dtype=torch.int32, device=device)
             st = L.gp_topk_decompress_unsorted(indices.data_ptr(), ib, values.data_ptr(), code, k, d, out.data_ptr(),
                                                out_code, scratch.data_ptr(), err.data_ptr(), sp)
             raise_for_status(st, "gp_topk_decompress_unsorted", indices)
-            flag = int(err.item())
+            flag = _Flags.read(err)
         if flag & _lib.FLAG_OUT_OF_RANGE:
             raise IndexOutOfRange(indices)
     return out

@@ -119,28 +119,27 @@ int gp_wire_bytes(int64_t d, double ratio, int64_t* bytes_out) {
 
 size_t gp_topk_workspace_bytes(int64_t d, int dtype) {
   if (d < 0) d = 0;
-  return gp::compress_workspace_layout((uint64_t)d, dtype, gp::kMaxGrid, nullptr);
+  return gp::compress_workspace_layout((uint64_t)d, dtype, nullptr);
 }
 
 int gp_workspace_init(void* ws, size_t ws_bytes, void* stream) {
   if (!ws) return GP_ERR_INVALID_ARGUMENT;
-  gp::WsLayout l;
-  gp::compress_workspace_layout(0, 0, gp::kMaxGrid, &l);
-  const size_t n = ws_bytes < l.lists ? ws_bytes : l.lists;  // only state that must start zeroed
-  return cudaMemsetAsync(ws, 0, n, as_stream(stream)) == cudaSuccess ? GP_OK : GP_ERR_CUDA;
+  // the whole buffer (the state regions' sizes depend on the d it was sized
+  // for); once: every call leaves the state it uses zeroed
+  return cudaMemsetAsync(ws, 0, ws_bytes, as_stream(stream)) == cudaSuccess ? GP_OK : GP_ERR_CUDA;
 }
 
 static int compress_impl(const void* x, int dtype, int64_t d, int64_t k, void* idx_out, int idx_bytes,
                          void* val_out, int val_dtype, void* val2_out, void* header_out, void* ws, size_t ws_bytes,
-                         void* stream, int max_ctas) {
+                         void* stream, int max_ctas, const int64_t* k_dev = nullptr, uint32_t* err = nullptr) {
   if (d <= 0) return GP_ERR_EMPTY_VECTOR;
-  if (!x || !idx_out || !val_out || !ws) return GP_ERR_INVALID_ARGUMENT;
+  if (!x || !idx_out || (!val_out && !k_dev) || !ws) return GP_ERR_INVALID_ARGUMENT;
   if (dtype < 0 || dtype > 2) return GP_ERR_INVALID_ARGUMENT;
   if (d >= (int64_t)1 << 31 || k < 1 || k > d) return GP_ERR_INVALID_ARGUMENT;
   if (idx_bytes != 4 && idx_bytes != 8) return GP_ERR_INVALID_ARGUMENT;
   if (val_dtype != GP_DTYPE_F32 && val_dtype != dtype) return GP_ERR_INVALID_ARGUMENT;
   gp::WsLayout l;
-  const size_t need = gp::compress_workspace_layout((uint64_t)d, dtype, gp::kMaxGrid, &l);
+  const size_t need = gp::compress_workspace_layout((uint64_t)d, dtype, &l);
   if (ws_bytes < need) return GP_ERR_INVALID_ARGUMENT;
   gp::DeviceInfo dev;
   if (device_info(&dev)) return GP_ERR_CUDA;
@@ -165,6 +164,9 @@ static int compress_impl(const void* x, int dtype, int64_t d, int64_t k, void* i
   a.lists = base + l.lists;
   a.aligned = ((uintptr_t)x % 32) == 0;
   a.dbg = g_debug_stamps;
+  a.k_dev = reinterpret_cast<const long long*>(k_dev);
+  a.frame_vals = k_dev != nullptr && val_out == nullptr;
+  a.err = err;
   return gp::launch_compress(dtype, a, dev, as_stream(stream));
 }
 
@@ -190,6 +192,17 @@ int gp_topk_compress_frame_ctas(const void* x, int dtype, int64_t d, int64_t k, 
                        GP_DTYPE_F32, nullptr, f, ws, ws_bytes, stream, max_ctas);
 }
 
+int gp_topk_compress_frame_dk(const void* x, int dtype, int64_t d, const int64_t* k_dev, int64_t k_cap,
+                              void* frame_out, uint32_t* d_err_flag, void* ws, size_t ws_bytes, void* stream,
+                              int max_ctas) {
+  if (!frame_out || !k_dev || ((uintptr_t)frame_out % 8) != 0 || max_ctas < 0) return GP_ERR_INVALID_ARGUMENT;
+  if (k_cap < 1 || k_cap > d) return GP_ERR_INVALID_ARGUMENT;
+  unsigned char* f = static_cast<unsigned char*>(frame_out);
+  // k_cap sizes the launch-independent checks; the kernel reads k and places the values after the k indices
+  return compress_impl(x, dtype, d, k_cap, f + GP_FRAME_HEADER_BYTES, 8, nullptr, GP_DTYPE_F32, nullptr, f, ws,
+                       ws_bytes, stream, max_ctas, k_dev, d_err_flag);
+}
+
 int gp_topk_compress_frame(const void* x, int dtype, int64_t d, int64_t k, void* frame_out, void* ws,
                            size_t ws_bytes, void* stream) {
   return gp_topk_compress_frame_ctas(x, dtype, d, k, frame_out, ws, ws_bytes, stream, 0);
@@ -197,16 +210,17 @@ int gp_topk_compress_frame(const void* x, int dtype, int64_t d, int64_t k, void*
 
 static int decompress_common(const void* idx, int idx_bytes, const void* vals, int val_dtype, int64_t k, int64_t d,
                              void* out, int out_dtype, int mode, uint32_t* d_err_flag, void* stream,
-                             void* scratch) {
+                             void* scratch, const void* hdr = nullptr, int dev_k = 0) {
   if (k < 0 || d < 0) return GP_ERR_INVALID_ARGUMENT;
   if (idx_bytes != 4 && idx_bytes != 8) return GP_ERR_INVALID_ARGUMENT;
   if (val_dtype < 0 || val_dtype > 2 || out_dtype < 0 || out_dtype > 2) return GP_ERR_INVALID_ARGUMENT;
   if (mode != 0 && mode != 1) return GP_ERR_INVALID_ARGUMENT;
-  if (!d_err_flag || (k > 0 && (!idx || !vals)) || (d > 0 && !out)) return GP_ERR_INVALID_ARGUMENT;
+  if (!d_err_flag || (k > 0 && (!idx || (!vals && !dev_k))) || (d > 0 && !out)) return GP_ERR_INVALID_ARGUMENT;
   if (d == 0 && k > 0) return GP_ERR_INDEX_OUT_OF_RANGE;  // every index is >= d
   gp::DeviceInfo dev;
   if (device_info(&dev)) return GP_ERR_CUDA;
-  gp::DecompressArgs a = {idx, idx_bytes == 8, vals, val_dtype, k, d, out, out_dtype, mode, d_err_flag, g_debug_dec};
+  gp::DecompressArgs a = {idx, idx_bytes == 8, vals, val_dtype, k, d, out, out_dtype, mode, d_err_flag, g_debug_dec,
+                          static_cast<const unsigned long long*>(hdr), dev_k};
   if (scratch) return gp::launch_decompress_unsorted(a, scratch, dev, as_stream(stream));
   return gp::launch_decompress(a, dev, as_stream(stream));
 }
@@ -220,8 +234,93 @@ int gp_topk_decompress_frame(const void* frame, int64_t k, int64_t d, void* out,
                              uint32_t* d_err_flag, void* stream) {
   if (!frame || ((uintptr_t)frame % 8) != 0) return GP_ERR_INVALID_ARGUMENT;
   const unsigned char* f = static_cast<const unsigned char*>(frame);
+  // the frame's own {d, k} header is checked against (d, k) in the same launch (GP_FLAG_HEADER)
   return decompress_common(f + GP_FRAME_HEADER_BYTES, 8, f + GP_FRAME_HEADER_BYTES + 8 * k, GP_DTYPE_F32, k, d, out,
-                           out_dtype, mode, d_err_flag, stream, nullptr);
+                           out_dtype, mode, d_err_flag, stream, nullptr, f, 0);
+}
+
+int gp_topk_decompress_frame_dk(const void* frame, int64_t d, int64_t k_cap, void* out, int out_dtype, int mode,
+                                uint32_t* d_err_flag, void* stream) {
+  if (!frame || ((uintptr_t)frame % 8) != 0 || k_cap < 1) return GP_ERR_INVALID_ARGUMENT;
+  const unsigned char* f = static_cast<const unsigned char*>(frame);
+  return decompress_common(f + GP_FRAME_HEADER_BYTES, 8, nullptr, GP_DTYPE_F32, k_cap, d, out, out_dtype, mode,
+                           d_err_flag, stream, nullptr, f, 1);
+}
+
+// ---- standalone frame pack / unpack (SparsePayload.to_bytes / from_bytes, compressor.py:39-53)
+namespace {
+__device__ __forceinline__ float val_as_f32(const void* v, int dt, int64_t j) {
+  if (dt == GP_DTYPE_F32) return static_cast<const float*>(v)[j];
+  if (dt == GP_DTYPE_BF16) return __uint_as_float((uint32_t)static_cast<const uint16_t*>(v)[j] << 16);
+  return __double2float_rn(static_cast<const double*>(v)[j]);
+}
+
+__global__ void pack_frame_kernel(const void* idx, int idx64, const void* vals, int val_dtype, int64_t k, int64_t d,
+                                  unsigned char* frame) {
+  unsigned long long* h = reinterpret_cast<unsigned long long*>(frame);
+  int64_t* fi = reinterpret_cast<int64_t*>(frame + GP_FRAME_HEADER_BYTES);
+  float* fv = reinterpret_cast<float*>(frame + GP_FRAME_HEADER_BYTES + 8 * k);
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    h[0] = (unsigned long long)d;
+    h[1] = (unsigned long long)k;
+  }
+  for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < k; j += (int64_t)gridDim.x * blockDim.x) {
+    fi[j] = idx64 ? static_cast<const int64_t*>(idx)[j] : (int64_t) static_cast<const int32_t*>(idx)[j];
+    fv[j] = val_as_f32(vals, val_dtype, j);
+  }
+}
+
+// k comes from the frame header (device memory); frames with k > k_cap or a
+// header other than {d_expect, .} (d_expect >= 0) raise GP_FLAG_HEADER and
+// unpack nothing.  hdr_out (nullable) receives the header as read.
+__global__ void unpack_frame_kernel(const unsigned char* frame, int64_t k_cap, int64_t d_expect, int64_t* idx_out,
+                                    void* vals_out, int val_dtype, int64_t* hdr_out, uint32_t* err) {
+  const unsigned long long hd = reinterpret_cast<const unsigned long long*>(frame)[0];
+  const unsigned long long hk = reinterpret_cast<const unsigned long long*>(frame)[1];
+  const bool ok = hk <= (unsigned long long)k_cap && (d_expect < 0 || hd == (unsigned long long)d_expect);
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    if (hdr_out) {
+      hdr_out[0] = (int64_t)hd;
+      hdr_out[1] = (int64_t)hk;
+    }
+    if (!ok && err) atomicOr(err, GP_FLAG_HEADER);
+  }
+  if (!ok) return;
+  const int64_t k = (int64_t)hk;
+  const int64_t* fi = reinterpret_cast<const int64_t*>(frame + GP_FRAME_HEADER_BYTES);
+  const float* fv = reinterpret_cast<const float*>(frame + GP_FRAME_HEADER_BYTES + 8 * k);
+  for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < k; j += (int64_t)gridDim.x * blockDim.x) {
+    idx_out[j] = fi[j];
+    const float v = fv[j];
+    if (val_dtype == GP_DTYPE_F64) static_cast<double*>(vals_out)[j] = (double)v;
+    else if (val_dtype == GP_DTYPE_F32) static_cast<float*>(vals_out)[j] = v;
+    else static_cast<uint16_t*>(vals_out)[j] = (uint16_t)(__float_as_uint(v) >> 16);  // exact for bf16-valued frames
+  }
+}
+
+unsigned frame_grid(int64_t k) {
+  const int64_t b = (k + 255) / 256;
+  return (unsigned)(b < 1 ? 1 : (b > 1184 ? 1184 : b));
+}
+}  // namespace
+
+int gp_pack_frame(const void* idx, int idx_bytes, const void* vals, int val_dtype, int64_t k, int64_t d,
+                  void* frame_out, void* stream) {
+  if (!frame_out || ((uintptr_t)frame_out % 8) != 0 || k < 0 || d < 0) return GP_ERR_INVALID_ARGUMENT;
+  if ((idx_bytes != 4 && idx_bytes != 8) || val_dtype < 0 || val_dtype > 2) return GP_ERR_INVALID_ARGUMENT;
+  if (k > 0 && (!idx || !vals)) return GP_ERR_INVALID_ARGUMENT;
+  pack_frame_kernel<<<frame_grid(k), 256, 0, as_stream(stream)>>>(idx, idx_bytes == 8, vals, val_dtype, k, d,
+                                                                  static_cast<unsigned char*>(frame_out));
+  return cudaGetLastError() == cudaSuccess ? GP_OK : GP_ERR_CUDA;
+}
+
+int gp_unpack_frame(const void* frame, int64_t k_cap, int64_t d_expect, int64_t* idx_out, void* vals_out,
+                    int val_dtype, int64_t* hdr_out, uint32_t* d_err_flag, void* stream) {
+  if (!frame || ((uintptr_t)frame % 8) != 0 || k_cap < 0 || val_dtype < 0 || val_dtype > 2) return GP_ERR_INVALID_ARGUMENT;
+  if (k_cap > 0 && (!idx_out || !vals_out)) return GP_ERR_INVALID_ARGUMENT;
+  unpack_frame_kernel<<<frame_grid(k_cap), 256, 0, as_stream(stream)>>>(
+      static_cast<const unsigned char*>(frame), k_cap, d_expect, idx_out, vals_out, val_dtype, hdr_out, d_err_flag);
+  return cudaGetLastError() == cudaSuccess ? GP_OK : GP_ERR_CUDA;
 }
 
 int gp_topk_decompress_unsorted(const void* idx, int idx_bytes, const void* vals, int val_dtype, int64_t k,

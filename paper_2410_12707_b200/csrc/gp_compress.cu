@@ -276,12 +276,13 @@ __device__ __forceinline__ bool warp_cross_desc(const uint32_t* hist, int top, u
 // output
 
 template <class Tr>
-__device__ __forceinline__ void write_out(const CompressArgs& a, uint32_t pos, uint32_t idx, typename Tr::Bits b) {
+__device__ __forceinline__ void write_out(const CompressArgs& a, void* val_out, uint32_t pos, uint32_t idx,
+                                          typename Tr::Bits b) {
   using Elem = typename Tr::Elem;
   if (a.idx64) reinterpret_cast<int64_t*>(a.idx_out)[pos] = (int64_t)idx;
   else reinterpret_cast<int32_t*>(a.idx_out)[pos] = (int32_t)idx;
-  if (a.val_f32) reinterpret_cast<float*>(a.val_out)[pos] = Tr::to_f32(b);
-  else reinterpret_cast<Elem*>(a.val_out)[pos] = (Elem)b;
+  if (a.val_f32) reinterpret_cast<float*>(val_out)[pos] = Tr::to_f32(b);
+  else reinterpret_cast<Elem*>(val_out)[pos] = (Elem)b;
   if (a.val2_out) reinterpret_cast<Elem*>(a.val2_out)[pos] = (Elem)b;
 }
 
@@ -359,7 +360,35 @@ __global__ void __launch_bounds__(kCompressThreads, 1) compress_kernel(const Com
 
   const uint32_t G = gridDim.x, c = blockIdx.x, tid = threadIdx.x;
   const uint32_t lane = tid & 31, w = tid >> 5;
-  const uint32_t d = a.d, k = a.k;
+  const uint32_t d = a.d;
+  uint32_t k = a.k;
+  void* val_out = a.val_out;
+  if (a.k_dev != nullptr) {
+    // device-resident k (an on-device AdaTopK plan): every CTA reads the same
+    // value, so an invalid k ends every CTA here (no grid barrier is reached)
+    const long long kk = __ldg(a.k_dev);
+    if (kk < 1 || kk > (long long)a.k || kk > (long long)d) {
+      if (c == 0 && tid == 0) {
+        if (a.err != nullptr) atomicOr(a.err, kFlagBadK);
+        if (a.header != nullptr) {
+          a.header[0] = (unsigned long long)d;
+          a.header[1] = ~0ull;  // an invalid frame: the receiver flags it
+        }
+      }
+      return;
+    }
+    k = (uint32_t)kk;
+    if (a.frame_vals) val_out = reinterpret_cast<unsigned char*>(a.idx_out) + (a.idx64 ? 8ull : 4ull) * k;
+    if (k == d) {  // ratio <= 1: every element kept, in index order (the pass-through)
+      if (a.header != nullptr && c == 0 && tid == 0) {
+        a.header[0] = (unsigned long long)d;
+        a.header[1] = (unsigned long long)k;
+      }
+      for (uint32_t i = c * blockDim.x + tid; i < d; i += gridDim.x * blockDim.x)
+        write_out<Tr>(a, val_out, i, i, load_bits<Tr>(a.x, i));
+      return;
+    }
+  }
   const uint32_t unit = c * 32u + w;
   const uint32_t u0 = (uint32_t)min((uint64_t)unit * a.W, (uint64_t)d);
   const uint32_t u1 = (uint32_t)min((uint64_t)u0 + a.W, (uint64_t)d);
@@ -1064,15 +1093,15 @@ __global__ void __launch_bounds__(kCompressThreads, 1) compress_kernel(const Com
         if constexpr (decltype(frame_out)::value) {  // reference frame: i64 indices, f32 values
           if (s0) {
             reinterpret_cast<int64_t*>(a.idx_out)[p] = (int64_t)i0;
-            reinterpret_cast<float*>(a.val_out)[p] = Tr::to_f32(b0);
+            reinterpret_cast<float*>(val_out)[p] = Tr::to_f32(b0);
           }
           if (s1) {
             reinterpret_cast<int64_t*>(a.idx_out)[p + s0] = (int64_t)i1;
-            reinterpret_cast<float*>(a.val_out)[p + s0] = Tr::to_f32(b1);
+            reinterpret_cast<float*>(val_out)[p + s0] = Tr::to_f32(b1);
           }
         } else {
-          if (s0) write_out<Tr>(a, p, i0, b0);
-          if (s1) write_out<Tr>(a, p + s0, i1, b1);
+          if (s0) write_out<Tr>(a, val_out, p, i0, b0);
+          if (s1) write_out<Tr>(a, val_out, p + s0, i1, b1);
         }
         o += __popc(q0) + __popc(q1);
       });
@@ -1166,7 +1195,7 @@ __global__ void __launch_bounds__(kCompressThreads, 1) compress_kernel(const Com
       const uint32_t em = __ballot_sync(kFull, iseq);
       const bool sel = valid && (kk > T || (iseq && er + __popc(em & lanemask_lt()) < need_eq));
       const uint32_t sm = __ballot_sync(kFull, sel);
-      if (sel) write_out<Tr>(a, o + __popc(sm & lanemask_lt()), idx, b);
+      if (sel) write_out<Tr>(a, val_out, o + __popc(sm & lanemask_lt()), idx, b);
       o += __popc(sm);
       er += __popc(em);
     });
@@ -1202,7 +1231,7 @@ __global__ void __launch_bounds__(256) keep_all_kernel(const CompressArgs a) {
     a.header[1] = (unsigned long long)a.k;
   }
   for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < a.d; i += gridDim.x * blockDim.x)
-    write_out<Tr>(a, i, i, load_bits<Tr>(a.x, i));
+    write_out<Tr>(a, a.val_out, i, i, load_bits<Tr>(a.x, i));
 }
 
 // ---------------------------------------------------------------------------
@@ -1210,17 +1239,26 @@ __global__ void __launch_bounds__(256) keep_all_kernel(const CompressArgs a) {
 
 // Fine-histogram resolution: 16 bits up to 2^23 elements, +1 bit per doubling
 // (max 20), so the population of the threshold bin stays roughly constant.
-template <class Tr>
-static int fine_bits(uint64_t d) {
-  if (Tr::kDirectT) return 16;
+static int fine_bits_for(bool direct_t, uint64_t d) {
+  if (direct_t) return 16;
   int fb = 16;
   while (fb < kFineBitsMax && (d >> (fb + 7)) != 0) ++fb;
   return fb;
 }
+template <class Tr>
+static int fine_bits(uint64_t d) {
+  return fine_bits_for(Tr::kDirectT, d);
+}
+
+// Largest cooperative grid a length-d compress can launch on any device
+// (launch_compress_t: G <= kMaxGridSpec and G <= ceil(d / kMinPerCta)).
+static uint32_t grid_bound(uint64_t d) {
+  return (uint32_t)std::min<uint64_t>(kMaxGridSpec, std::max<uint64_t>(1, (d + kMinPerCta - 1) / kMinPerCta));
+}
 
 template <class Tr>
 static int launch_compress_t(CompressArgs a, const DeviceInfo& dev, cudaStream_t stream) {
-  if (a.k == a.d) {
+  if (a.k == a.d && a.k_dev == nullptr) {
     const uint32_t blocks = (uint32_t)std::min<uint64_t>(((uint64_t)a.d + 255) / 256, (uint64_t)dev.num_sms * 8);
     keep_all_kernel<Tr><<<blocks, 256, 0, stream>>>(a);
     return cudaGetLastError() == cudaSuccess ? 0 : 5;
@@ -1269,24 +1307,33 @@ int launch_compress(int dtype, CompressArgs a, const DeviceInfo& dev, cudaStream
   }
 }
 
-size_t compress_workspace_layout(uint64_t d, int dtype, int gmax, WsLayout* out) {
+// Workspace of a length-d compress, sized by d: the fine histogram by the
+// fine-bit count the launcher picks for d (f32/f64 rule for every dtype), the
+// per-CTA regions by the largest grid d can get (grid_bound), the candidate
+// lists by d.  The regions that must stay zeroed (ctrl, histograms) come
+// first and grow with d only, so a workspace sized for d and zeroed once
+// serves every later call with d' <= d: the state regions of d' lie inside
+// those of d.
+size_t compress_workspace_layout(uint64_t d, int dtype, WsLayout* out) {
   const size_t entry = dtype == 2 ? 16 : 8;
   const size_t key = dtype == 2 ? 8 : 4;
+  const size_t gmax = grid_bound(d);
+  const size_t nfine = (size_t)1 << fine_bits_for(false, d);
   auto up = [](size_t v) { return (v + 255) & ~(size_t)255; };
   WsLayout l;
   size_t off = 0;
   l.ctrl = off;
   off = up(off + 256);
   l.hist1 = off;
-  off = up(off + (size_t)kHistCopies * kFineBinsMax * 4);
+  off = up(off + ((size_t)(kHistCopies - 1) * kFineBinsMax + nfine) * 4);  // replica r at r * kFineBinsMax
   l.hist_lvl = off;
   off = up(off + (size_t)8 * 256 * 4);
   l.cta_a = off;
-  off = up(off + (size_t)kMaxGrid * 4);
+  off = up(off + gmax * 4);
   l.cta_b = off;
-  off = up(off + (size_t)kMaxGrid * 4);
+  off = up(off + gmax * 4);
   l.fcreg = off;
-  off = up(off + (size_t)gmax * kFcCap * key);
+  off = up(off + gmax * kFcCap * key);
   l.lists = off;
   off = up(off + ((size_t)d + (size_t)gmax * 32 * 16) * entry);
   l.total = off;

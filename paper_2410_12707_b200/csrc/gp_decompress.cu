@@ -158,8 +158,21 @@ __device__ __forceinline__ bool pair_check_rest(const IT* __restrict__ idx, int6
 template <class IT, class VT, class OT>
 __global__ void __launch_bounds__(kDecThreads, kDecBlocksPerSm) decompress_kernel(
     const IT* __restrict__ idx, const VT* __restrict__ vals, int64_t k, int64_t d, int64_t chunk,
-    OT* __restrict__ out, int mode, uint32_t* err, unsigned long long* dbg) {
+    OT* __restrict__ out, int mode, uint32_t* err, unsigned long long* dbg, const unsigned long long* hdr, int dev_k) {
   constexpr int kTileElems = kTileBytes / (int)sizeof(OT);
+  if (hdr != nullptr) {  // the frame's {d, k} header against what the receiver expects
+    const unsigned long long hd = __ldg(hdr), hk = __ldg(hdr + 1);
+    const bool ok = hd == (unsigned long long)d &&
+                    (dev_k ? hk >= 1ull && hk <= (unsigned long long)k : hk == (unsigned long long)k);
+    if (!ok) {
+      if (blockIdx.x == 0 && threadIdx.x == 0) atomicOr(err, kFlagHeader);
+      k = 0;  // nothing is scattered: zeros (mode 0) or the untouched residual (mode 1)
+    } else if (dev_k) {
+      k = (int64_t)hk;
+      vals = reinterpret_cast<const VT*>(idx + k);  // reference frame: the values follow the k indices
+    }
+  }
+
   constexpr int kVecs = kTileBytes / 16;
 #define DSTAMP(i)                                                \
   do {                                                           \
@@ -227,7 +240,7 @@ __global__ void __launch_bounds__(kDecThreads, kDecBlocksPerSm) decompress_kerne
     // consume the early loads here (not at the end, where the compiler would
     // otherwise sink them into an extra serialized round trip)
     if (!(pa < pz)) bad = true;
-    if (blockIdx.x == 0 && tid == 0 && (first < 0 || last >= d)) atomicOr(err, 1u);
+    if (blockIdx.x == 0 && tid == 0 && (first < 0 || last >= d)) atomicOr(err, kFlagOutOfRange);
     const int below = __syncthreads_count(pv < o0);
     const int64_t p_first = probe_pos(0), p_last = probe_pos(kDecThreads - 1);
     if ((below == 0 && p_first > 0) || (below == kDecThreads && p_last < k - 1)) {
@@ -310,7 +323,7 @@ __global__ void __launch_bounds__(kDecThreads, kDecBlocksPerSm) decompress_kerne
   if (GP_DEC_TMA && tid == 0) bulk_wait_all();  // the stores must finish before the CTA's smem goes away
   DSTAMP(3);
   if (pair_check_rest(idx, pb + tid + kDecThreads, pe)) bad = true;
-  if (__syncthreads_or(bad) && tid == 0) atomicOr(err, 2u);
+  if (__syncthreads_or(bad) && tid == 0) atomicOr(err, kFlagUnsorted);
   DSTAMP(4);
 #undef DSTAMP
 }
@@ -326,7 +339,19 @@ __global__ void __launch_bounds__(kDecThreads, kDecBlocksPerSm) decompress_kerne
 template <class IT, class VT, class OT>
 __global__ void __launch_bounds__(kDecThreads, kDecBlocksPerSm) decompress_sparse_kernel(
     const IT* __restrict__ idx, const VT* __restrict__ vals, int64_t k, int64_t d, int64_t chunk,
-    OT* __restrict__ out, uint32_t* err) {
+    OT* __restrict__ out, uint32_t* err, const unsigned long long* hdr, int dev_k) {
+  if (hdr != nullptr) {  // the frame's {d, k} header against what the receiver expects
+    const unsigned long long hd = __ldg(hdr), hk = __ldg(hdr + 1);
+    const bool ok = hd == (unsigned long long)d &&
+                    (dev_k ? hk >= 1ull && hk <= (unsigned long long)k : hk == (unsigned long long)k);
+    if (!ok) {
+      if (blockIdx.x == 0 && threadIdx.x == 0) atomicOr(err, kFlagHeader);
+      k = 0;  // nothing is scattered: zeros (mode 0) or the untouched residual (mode 1)
+    } else if (dev_k) {
+      k = (int64_t)hk;
+      vals = reinterpret_cast<const VT*>(idx + k);  // reference frame: the values follow the k indices
+    }
+  }
   const uint32_t tid = threadIdx.x;
   const int64_t o0 = min((int64_t)blockIdx.x * chunk, d);
   const int64_t o1 = min(o0 + chunk, d);
@@ -364,7 +389,7 @@ __global__ void __launch_bounds__(kDecThreads, kDecBlocksPerSm) decompress_spars
   }
   if (k == 0) return;
   if (!(pa < pz)) bad = true;
-  if (blockIdx.x == 0 && tid == 0 && (first < 0 || last >= d)) atomicOr(err, 1u);
+  if (blockIdx.x == 0 && tid == 0 && (first < 0 || last >= d)) atomicOr(err, kFlagOutOfRange);
   __shared__ int64_t sh_lo;
   const int below = __syncthreads_count(pv < o0);  // also orders the fill before the scatter
   int64_t base;
@@ -390,7 +415,7 @@ __global__ void __launch_bounds__(kDecThreads, kDecBlocksPerSm) decompress_spars
     if (__syncthreads_or(past)) break;
   }
   if (pair_check_rest(idx, pb + tid + kDecThreads, pe)) bad = true;
-  if (__syncthreads_or(bad) && tid == 0) atomicOr(err, 2u);
+  if (__syncthreads_or(bad) && tid == 0) atomicOr(err, kFlagUnsorted);
 }
 
 // ---- general path
@@ -404,7 +429,7 @@ template <class IT>
 __global__ void winner_kernel(const IT* idx, int64_t k, int64_t d, int32_t* win, uint32_t* err) {
   for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < k; j += (int64_t)gridDim.x * blockDim.x) {
     const int64_t i = (int64_t)idx[j];
-    if (i < 0 || i >= d) atomicOr(err, 1u);
+    if (i < 0 || i >= d) atomicOr(err, kFlagOutOfRange);
     else atomicMax(&win[i], (int32_t)j);
   }
 }
@@ -439,10 +464,10 @@ static int run_fast(const DecompressArgs& a, const DeviceInfo& dev, cudaStream_t
   }
   if (a.mode == 0 && a.k * kSparseDensityInv <= a.d && a.d * (int64_t)sizeof(OT) <= kSparseMaxBytes) {
     decompress_sparse_kernel<IT, VT, OT><<<(unsigned)grid, kDecThreads, 0, s>>>(
-        (const IT*)a.idx, (const VT*)a.vals, a.k, a.d, chunk, (OT*)a.out, a.err);
+        (const IT*)a.idx, (const VT*)a.vals, a.k, a.d, chunk, (OT*)a.out, a.err, a.hdr, a.dev_k);
   } else {
     decompress_kernel<IT, VT, OT><<<(unsigned)grid, kDecThreads, kTileBufs * kTileBytes, s>>>(
-        (const IT*)a.idx, (const VT*)a.vals, a.k, a.d, chunk, (OT*)a.out, a.mode, a.err, a.dbg);
+        (const IT*)a.idx, (const VT*)a.vals, a.k, a.d, chunk, (OT*)a.out, a.mode, a.err, a.dbg, a.hdr, a.dev_k);
   }
   return cudaGetLastError() == cudaSuccess ? 0 : 5;
 }

@@ -32,6 +32,12 @@ constexpr int kCtrlMaxLoBin = 3;        // 1 + highest per-CTA watermark bin
 constexpr int kCtrlCands = 4;           // total candidates of stage 1
 constexpr int kCtrlMinLoBin = 5;        // ~(lowest per-CTA watermark bin), via atomicMax
 
+// asynchronous device error flags (include/adatopk.h GP_FLAG_*)
+constexpr uint32_t kFlagOutOfRange = 1u;
+constexpr uint32_t kFlagUnsorted = 2u;
+constexpr uint32_t kFlagHeader = 4u;
+constexpr uint32_t kFlagBadK = 8u;
+
 struct CompressArgs {
   const void* x;
   uint32_t d;
@@ -53,6 +59,12 @@ struct CompressArgs {
   int aligned;              // x is 32-byte aligned (256-bit row loads)
   int fb;                   // fine-histogram bits, set by the launcher
   unsigned long long* dbg;  // optional per-CTA stage timestamps (32 words per CTA)
+  // device-resident k (adaptive plans without a host round trip): when set,
+  // k = *k_dev, bounded by the capacity a.k; with frame_vals the values start
+  // right after the k indices (reference frame layout), so val_out is derived
+  const long long* k_dev;
+  int frame_vals;
+  uint32_t* err;            // GP_FLAG_BAD_K when *k_dev is outside [1, min(k_cap, d)]
 };
 
 struct WsLayout {
@@ -68,7 +80,7 @@ struct DeviceInfo {
 };
 
 int launch_compress(int dtype, CompressArgs a, const DeviceInfo& dev, cudaStream_t stream);
-size_t compress_workspace_layout(uint64_t d, int dtype, int gmax, WsLayout* out);
+size_t compress_workspace_layout(uint64_t d, int dtype, WsLayout* out);
 
 struct DecompressArgs {
   const void* idx;
@@ -82,6 +94,11 @@ struct DecompressArgs {
   int mode;
   uint32_t* err;
   unsigned long long* dbg;  // optional per-CTA stage timestamps (8 words per CTA)
+  // frame header {d, k} to validate (nullable): GP_FLAG_HEADER on a mismatch.
+  // dev_k: k is read from the header (bounded by the capacity a.k) and the
+  // values start right after the k indices.
+  const unsigned long long* hdr;
+  int dev_k;
 };
 
 int launch_decompress(const DecompressArgs& a, const DeviceInfo& dev, cudaStream_t stream);

@@ -309,6 +309,14 @@ class PipelineStats:
     dense_bytes: int = 0
 
 
+def _amp(device):
+    """bf16 autocast for the stage matmuls on a GPU; plain fp32 on CPU ranks (tests)."""
+    if torch.device(device).type == "cuda":
+        return torch.autocast("cuda", dtype=torch.bfloat16)
+    import contextlib
+    return contextlib.nullcontext()
+
+
 class VirtualPipeline:
     """All S stages in one process/GPU, compressing at every boundary (fill-drain)."""
 
@@ -343,7 +351,7 @@ class VirtualPipeline:
             x = mbs[m]
             for s in range(S):
                 inp = x if s == 0 else x.requires_grad_(True)
-                with torch.autocast("cuda", dtype=torch.bfloat16):
+                with _amp(self.device):
                     y = self.stages[s](inp, tgs[m] if s == S - 1 else None)
                 acts[m][s] = (inp, y)
                 if s < S - 1:
@@ -367,48 +375,149 @@ class VirtualPipeline:
         return loss
 
 
+class DevicePlan:
+    """Per-link k kept on the device (north_star item 4): Eq. 6 + select_k run
+    in the plan kernel (gp_adatopk_plan) into `k`, a CUDA int64 tensor, and the
+    compress kernels read their k from it, so re-planning every step needs no
+    host round trip.  Frames are sized for a host-known capacity per link,
+    `k_cap = select_k(d, ratio_floor)`; a planned k above it is clamped on the
+    device (`clamped` counts such links, read whenever the caller syncs) --
+    with measured NVSwitch links Eq. 6 gives every link r ~ 3r, far above the
+    floor.  The receiver reads k from each frame's header."""
+
+    def __init__(self, links: list, boundary: int, base_ratio: float, device, ratio_floor: Optional[float] = None):
+        self.links = list(links)
+        self.index = {lk: i for i, lk in enumerate(self.links)}
+        self.boundary, self.base_ratio, self.device = int(boundary), float(base_ratio), device
+        self.k_cap = select_k(self.boundary, ratio_floor if ratio_floor is not None else base_ratio)
+        n = len(self.links)
+        self.k = torch.full((n,), self.k_cap, dtype=torch.int64, device=device)
+        self.r = torch.zeros(n, dtype=torch.float64, device=device)
+        self.status = torch.zeros(1, dtype=torch.int32, device=device)
+        self.clamped = torch.zeros(1, dtype=torch.int64, device=device)
+        self._dl = torch.full((n,), self.boundary, dtype=torch.int64, device=device)
+
+    def replan(self, R: torch.Tensor) -> None:
+        """Eq. 6 from link times R (float64 CUDA tensor, one per link), stream-ordered, no host sync."""
+        from .compressor import _lib, _stream_handle
+        import ctypes
+
+        P = ctypes.POINTER
+        R = R.to(device=self.device, dtype=torch.float64).contiguous()
+        st = _lib.lib().gp_adatopk_plan(
+            ctypes.cast(R.data_ptr(), P(ctypes.c_double)), len(self.links), self.base_ratio,
+            ctypes.cast(self._dl.data_ptr(), P(ctypes.c_int64)), ctypes.cast(self.r.data_ptr(), P(ctypes.c_double)),
+            ctypes.cast(self.k.data_ptr(), P(ctypes.c_int64)), ctypes.cast(self.status.data_ptr(), P(ctypes.c_int32)),
+            _stream_handle(self.device))
+        if st != 0:
+            from .errors import raise_for_status
+            raise_for_status(st, "gp_adatopk_plan")
+        self.clamped += (self.k > self.k_cap).sum()
+        torch.clamp_(self.k, max=self.k_cap)
+
+    def k_slot(self, link) -> torch.Tensor:
+        i = self.index[link]
+        return self.k[i:i + 1]
+
+
+class _HostWork:
+    """A gloo P2P request on a host staging buffer; `wait()` copies a received buffer to the device."""
+
+    def __init__(self, work, host, dst=None):
+        self.work, self.host, self.dst = work, host, dst
+
+    def wait(self):
+        self.work.wait()
+        if self.dst is not None:
+            self.dst.copy_(self.host)
+        return True
+
+
 class DistPipeline:
-    """One stage per rank (torch.distributed, NCCL); fill-drain with compressed P2P."""
+    """One stage per rank (torch.distributed); fill-drain with compressed P2P.
+
+    `chain` maps pipeline stages to ranks (stage s runs on rank chain[s]; the
+    default is the identity); the OP-Fence schedule supplies it as its
+    device_chain (opfence.py:347-435).  `device` (default: the current CUDA
+    device) and `codec` make the same fill-drain logic runnable on CPU ranks
+    over gloo with a host codec, which the multi-rank CPU tests use.  With a
+    `dev_plan` the boundaries use device-resident k (DevicePlan).  The codec's
+    validation flag is read once at the end of every step.
+    """
 
     def __init__(self, cfg: GPT2Config, plan: Optional[CompressionPlan], micro_batch: int, seq_len: int,
-                 lr: float = 1e-4, seed: int = 0):
+                 lr: float = 1e-4, seed: int = 0, chain: Optional[list] = None, device=None, codec=None,
+                 dev_plan: Optional[DevicePlan] = None, bounds: Optional[list] = None, sdpa: bool = True):
         self.rank, self.S = dist.get_rank(), dist.get_world_size()
-        self.device = torch.device("cuda", torch.cuda.current_device())
+        self.chain = list(chain) if chain is not None else list(range(self.S))
+        if sorted(self.chain) != list(range(self.S)):
+            raise ValueError(f"chain {self.chain} is not a permutation of the {self.S} ranks")
+        self.s = self.chain.index(self.rank)  # this rank's stage
+        self.device = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
         self.cfg, self.plan, self.mb, self.T = cfg, plan, micro_batch, seq_len
-        self.stage = make_stage(cfg, self.rank, self.S, self.device, seed)
+        self.dev_plan = dev_plan
+        if bounds is None:
+            self.stage = make_stage(cfg, self.s, self.S, self.device, seed, sdpa)
+        else:
+            a, b = bounds[self.s]
+            self.stage = Stage(cfg, a, b, self.s == 0, self.s == self.S - 1, sdpa, seed).to(self.device)
         self.opt = torch.optim.AdamW(self.stage.parameters(), lr=lr)
-        self.codec = FrameCodec(self.device)
+        self.codec = codec if codec is not None else FrameCodec(self.device)
         self.shape = (micro_batch, seq_len, cfg.n_embd)
+        self.messages = []  # (direction, src_stage, dst_stage, micro_batch) in send order (tests)
+
+    def _amp(self):
+        return _amp(self.device)
 
     def _ratio(self, src, dst):
         return self.plan.ratio_for(src, dst) if self.plan is not None else 1.0
 
+    def _p2p(self, op, buf, peer_stage):
+        peer = self.chain[peer_stage]
+        if self.device.type == "cuda" and dist.get_backend() == "gloo":
+            # CUDA tensors over gloo (several ranks sharing one GPU in the
+            # tests): the frame is staged through host memory
+            if op is dist.isend:
+                h = buf.cpu()
+                return _HostWork(dist.isend(h, peer), h)
+            h = torch.empty(buf.shape, dtype=buf.dtype)
+            return _HostWork(dist.irecv(h, peer), h, buf)
+        if _P2P_BATCHED and self.device.type == "cuda":
+            return dist.batch_isend_irecv([dist.P2POp(op, buf, peer)])[0]
+        return op(buf, peer)
+
     def _send(self, x: torch.Tensor, dst: int):
-        r = self._ratio(self.rank, dst)
-        buf = x.detach().contiguous() if r <= 1.0 else self.codec.compress(x.detach().contiguous(), r)
-        if _P2P_BATCHED:
-            return dist.batch_isend_irecv([dist.P2POp(dist.isend, buf, dst)])[0], buf
-        return dist.isend(buf, dst), buf
+        """Send stage self.s's tensor to stage dst (link keys are stage indices)."""
+        link = (self.s, dst)
+        if self.dev_plan is not None and link in self.dev_plan.index:
+            buf = self.codec.compress_dk(x.detach().contiguous(), self.dev_plan.k_slot(link), self.dev_plan.k_cap)
+        else:
+            r = self._ratio(*link)
+            buf = x.detach().contiguous() if r <= 1.0 else self.codec.compress(x.detach().contiguous(), r)
+        return self._p2p(dist.isend, buf, dst), buf
 
     def _recv(self, src: int) -> torch.Tensor:
-        r = self._ratio(src, self.rank)
+        link = (src, self.s)
         out = torch.empty(self.shape, device=self.device)
+        if self.dev_plan is not None and link in self.dev_plan.index:
+            k_cap = self.dev_plan.k_cap
+            buf = torch.empty(16 + 12 * k_cap, dtype=torch.uint8, device=self.device)
+            self._p2p(dist.irecv, buf, src).wait()
+            return self.codec.decompress_dk(buf, out, k_cap)
+        r = self._ratio(*link)
         buf = out if r <= 1.0 else torch.empty(frame_bytes(out.numel(), r), dtype=torch.uint8, device=self.device)
-        if _P2P_BATCHED:
-            dist.batch_isend_irecv([dist.P2POp(dist.irecv, buf, src)])[0].wait()
-        else:
-            dist.irecv(buf, src).wait()
+        self._p2p(dist.irecv, buf, src).wait()
         return out if r <= 1.0 else self.codec.decompress(buf, out, r)
 
     def forward_only(self, tokens: torch.Tensor, targets: torch.Tensor, n_micro: int):
         """The FP half of a step (fill phase, no backward): what Eq. 3 / Eq. 7 model."""
-        s, S = self.rank, self.S
+        s, S = self.s, self.S
         mbs, tgs = tokens.chunk(n_micro), targets.chunk(n_micro)
         pending = []
         with torch.no_grad():
             for m in range(n_micro):
                 inp = mbs[m] if s == 0 else self._recv(s - 1)
-                with torch.autocast("cuda", dtype=torch.bfloat16):
+                with self._amp():
                     y = self.stage(inp, tgs[m] if s == S - 1 else None)
                 if s < S - 1:
                     pending.append(self._send(y, s + 1))
@@ -417,14 +526,14 @@ class DistPipeline:
 
     def stage_fp_time(self, tokens: torch.Tensor, targets: torch.Tensor, reps: int = 5) -> float:
         """C_d: this stage's forward time for one micro-batch (s, CUDA events, median)."""
-        x = tokens[: self.mb] if self.rank == 0 else torch.randn(self.shape, device=self.device)
-        tg = targets[: self.mb] if self.rank == self.S - 1 else None
+        x = tokens[: self.mb] if self.s == 0 else torch.randn(self.shape, device=self.device)
+        tg = targets[: self.mb] if self.s == self.S - 1 else None
         ts = []
         with torch.no_grad():
             for _ in range(reps + 1):
                 a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                 a.record()
-                with torch.autocast("cuda", dtype=torch.bfloat16):
+                with self._amp():
                     self.stage(x, tg)
                 b.record()
                 torch.cuda.synchronize()
@@ -432,17 +541,22 @@ class DistPipeline:
         ts = sorted(ts[1:])
         return ts[len(ts) // 2]
 
-    def step(self, tokens: torch.Tensor, targets: torch.Tensor, n_micro: int):
-        s, S = self.rank, self.S
+    def step(self, tokens: torch.Tensor, targets: torch.Tensor, n_micro: int, check: bool = True):
+        """One GPipe fill-drain iteration (executor.py:376-411): every micro-batch
+        forward (activations to the next stage, _send_activation :248-274), then
+        every micro-batch backward (gradients to the previous stage,
+        _send_gradient :276-297), then the optimizer step."""
+        s, S = self.s, self.S
         mbs, tgs = tokens.chunk(n_micro), targets.chunk(n_micro)
         pending, saved, losses = [], [], []
         for m in range(n_micro):  # fill
             inp = mbs[m] if s == 0 else self._recv(s - 1).requires_grad_(True)
-            with torch.autocast("cuda", dtype=torch.bfloat16):
+            with self._amp():
                 y = self.stage(inp, tgs[m] if s == S - 1 else None)
             saved.append((inp, y))
             if s < S - 1:
                 pending.append(self._send(y, s + 1))
+                self.messages.append(("fp", s, s + 1, m))
             else:
                 losses.append(y.detach())
         for m in range(n_micro):  # drain
@@ -453,12 +567,15 @@ class DistPipeline:
                 y.backward(self._recv(s + 1))
             if s > 0:
                 pending.append(self._send(inp.grad, s - 1))
+                self.messages.append(("bp", s, s - 1, m))
         for w, _buf in pending:
             w.wait()
         self.opt.step()
         self.opt.zero_grad(set_to_none=True)
         loss = torch.stack(losses).mean() if losses else torch.zeros((), device=self.device)
-        dist.broadcast(loss, S - 1)
+        dist.broadcast(loss, self.chain[S - 1])
+        if check and hasattr(self.codec, "check"):
+            self.codec.check()  # one flag read per step: a corrupt received frame raises here
         return float(loss)
 
 

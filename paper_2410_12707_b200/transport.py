@@ -53,8 +53,10 @@ def frame_bytes(d: int, ratio: float) -> int:
 class FrameCodec:
     """Device-side compress-to-frame / decompress-from-frame with reusable buffers.
 
-    The hot path of a pipeline stage boundary: no host synchronisation, errors
-    are accumulated in a device flag (`check()` reads it).
+    The hot path of a pipeline stage boundary: no host synchronisation.  Every
+    decompress checks the received frame on the device (index range, strict
+    order, and its {d, k} header against the receiver's own (d, k)); failures
+    accumulate in a device flag that `check()` reads once per step.
     """
 
     device: torch.device
@@ -94,13 +96,50 @@ class FrameCodec:
         raise_for_status(st, "gp_topk_decompress_frame")
         return out
 
+    # ---- device-resident k (north_star item 4): k comes from device memory
+    # (e.g. the on-device Eq. 6 plan), frames are sized for a host-known
+    # capacity k_cap, and the receiver reads k from the frame header.
+
+    def compress_dk(self, x: torch.Tensor, k_dev: torch.Tensor, k_cap: int,
+                    frame: Optional[torch.Tensor] = None) -> torch.Tensor:
+        """Compress with k = k_dev[0] (int64 CUDA scalar) into a 16 + 12*k_cap byte frame."""
+        with torch.cuda.device(self.device):
+            flat = x.reshape(-1)
+            if not flat.is_contiguous():
+                flat = flat.contiguous()
+            d = flat.numel()
+            if frame is None:
+                frame = torch.empty(16 + 12 * k_cap, dtype=torch.uint8, device=self.device)
+            code = _DTYPE_CODE[flat.dtype]
+            sp = _stream_handle(self.device)
+            ws, wsb = _Workspace.get(self.device, sp, d, code)
+            st = _lib.lib().gp_topk_compress_frame_dk(flat.data_ptr(), code, d, k_dev.data_ptr(), k_cap,
+                                                      frame.data_ptr(), self.err.data_ptr(), ws, wsb, sp, 0)
+            raise_for_status(st, "gp_topk_compress_frame_dk")
+            return frame
+
+    def decompress_dk(self, frame: torch.Tensor, out: torch.Tensor, k_cap: int, accumulate: bool = False):
+        """Decompress a frame whose k is read from its own header (1 <= k <= k_cap)."""
+        with torch.cuda.device(self.device):
+            st = _lib.lib().gp_topk_decompress_frame_dk(frame.data_ptr(), out.numel(), k_cap, out.data_ptr(),
+                                                        _DTYPE_CODE[out.dtype], 1 if accumulate else 0,
+                                                        self.err.data_ptr(), _stream_handle(self.device))
+            raise_for_status(st, "gp_topk_decompress_frame_dk")
+            return out
+
     def check(self):
+        """Read the accumulated device flag (one host sync) and raise on any failure."""
         flag = int(self.err.item())
-        self.err.zero_()
+        if flag:
+            self.err.zero_()
         if flag & _lib.FLAG_OUT_OF_RANGE:
             raise IndexOutOfRange("received frame holds an index outside [0, d)")
         if flag & _lib.FLAG_UNSORTED:
             raise ValueError("received frame indices are not strictly increasing")
+        if flag & _lib.FLAG_HEADER:
+            raise ValueError("received frame header {d, k} disagrees with the receiver's (d, k)")
+        if flag & _lib.FLAG_BAD_K:
+            raise ValueError("device-resident k outside [1, min(k_cap, d)]")
 
 
 class StageLink:
@@ -111,7 +150,10 @@ class StageLink:
     group (`batch_isend_irecv`, so neighbouring stages cannot deadlock),
     waits, and decompresses every received frame into its destination buffer.
     The codec is pluggable (default: the sm_100a `FrameCodec`); frame sizes are
-    derived from (d, ratio) on both ends.
+    derived from (d, ratio) on both ends, and each received frame's header is
+    checked against them on the device.  With `check=True` (default) the
+    codec's flag is read once at the end of the exchange (one host sync per
+    exchange, not per frame) and a corrupt or mismatched frame raises.
     """
 
     def __init__(self, device: torch.device, group=None, codec=None):
@@ -119,7 +161,7 @@ class StageLink:
         self.group = group
         self.codec = codec if codec is not None else FrameCodec(device)
 
-    def exchange(self, sends, recvs):
+    def exchange(self, sends, recvs, check: bool = True):
         """sends: [(tensor, ratio, dst)]; recvs: [(out_tensor, ratio, src)] -> decompressed outs."""
         ops, frames_in = [], []
         for x, ratio, dst in sends:
@@ -142,6 +184,8 @@ class StageLink:
             if ratio > 1.0:
                 self.codec.decompress(buf, out, ratio)
             outs.append(out)
+        if check and hasattr(self.codec, "check"):
+            self.codec.check()
         return outs
 
 

@@ -163,3 +163,24 @@ def test_status_mapping():
         with pytest.raises(exc):
             raise_for_status(code)
     raise_for_status(0)
+
+
+def test_workspace_scales_with_d():
+    """gp_topk_workspace_bytes is sized by d (fine histogram by the fine-bit
+    count d gets, per-CTA regions by the grid d can get, lists by d): a tiny
+    vector needs well under 8 MB, and the state regions of a shorter vector
+    lie inside those of a longer one, so a workspace serves every d' <= d."""
+    L = _lib.lib()
+    tiny = L.gp_topk_workspace_bytes(1000, 0)
+    assert tiny <= 1 << 20, tiny
+    c1 = 8 * 1024 * 768
+    ws_c1 = L.gp_topk_workspace_bytes(c1, 0)
+    assert ws_c1 <= 2.5 * 4 * c1, ws_c1  # was 3.7x the input in round 1 (fcreg sized for 1024 CTAs)
+    prev = 0
+    for d in (1, 1000, 16384, 10**5, 10**6, c1, 5 * 10**7, 2**31 - 1):
+        for dt in (0, 1, 2):
+            n = L.gp_topk_workspace_bytes(d, dt)
+            assert n >= 8 * d
+        n = L.gp_topk_workspace_bytes(d, 0)
+        assert n >= prev
+        prev = n

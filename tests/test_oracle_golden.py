@@ -37,10 +37,11 @@ def test_oracle_round_trip_and_decompress():
         vals, idx, d = O.from_bytes(frame)
         dense = O.topk_decompress(vals, idx, d)
         assert dense.dtype == np.float64 and dense.size == d
+        # the golden frame decodes to the oracle's own decompress of a fresh
+        # compress, bit for bit (values widened to float64 as from_bytes does)
         v2, i2, _ = O.topk_compress(x, ratio)
-        ref = O.topk_decompress(v2, i2, d)
-        assert np.array_equal(ref.view(np.uint32) if ref.dtype == np.float32 else ref,
-                              ref.view(np.uint32) if ref.dtype == np.float32 else ref)
+        ref = O.topk_decompress(v2, i2, d).astype(np.float64)
+        assert np.array_equal(dense.view(np.uint64), ref.view(np.uint64)), name
         np.testing.assert_array_equal(dense[idx], x[idx].astype(np.float64))
 
 

@@ -95,9 +95,67 @@ def _run(world, backend):
     return res
 
 
-def test_ring_exchange_gloo_world2():
-    res = _run(2, "gloo")
-    assert res == {0: True, 1: True}, res
+@pytest.mark.parametrize("world", [2, 4, 8])
+def test_ring_exchange_gloo(world):
+    """Every rank sends to rank+1 and receives from rank-1 in one grouped
+    exchange: world 2, 4 and 8 (the 8-stage pipeline's link count)."""
+    res = _run(world, "gloo")
+    assert res == {r: True for r in range(world)}, res
+
+
+def _corrupt_worker(rank, world, port, q):
+    """A received frame whose header disagrees with the receiver's (d, k), or
+    whose index leaves [0, d), raises at the end of the exchange."""
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    try:
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+        out = torch.empty(1000)
+        got = []
+        for case in ("header", "index"):
+            if rank == 0:
+                frame = bytearray(O.compress_frame(np.arange(1000, dtype=np.float32), 10.0))
+                if case == "header":
+                    frame[8:16] = (50).to_bytes(8, "little")  # k = 50, the receiver expects 100
+                else:
+                    frame[16:24] = (5000).to_bytes(8, "little")  # index 5000 >= d
+                dist.send(torch.frombuffer(frame, dtype=torch.uint8), 1)
+            else:
+                buf = torch.empty(T.frame_bytes(1000, 10.0), dtype=torch.uint8)
+                dist.recv(buf, 0)
+                try:
+                    CheckingOracleCodec().decompress(buf, out, 10.0)
+                    got.append("no error")
+                except (ValueError, O.IndexOutOfRange) as e:
+                    got.append(type(e).__name__)
+        dist.barrier()
+        dist.destroy_process_group()
+        q.put((rank, got))
+    except Exception as e:
+        q.put((rank, repr(e)))
+
+
+class CheckingOracleCodec(OracleCodec):
+    """The oracle codec with the receiver-side frame checks the device codec does."""
+
+    def decompress(self, frame, out, ratio):
+        d, k = out.numel(), O.select_k(out.numel(), ratio)
+        hd, hk = (int(v) for v in np.frombuffer(frame.numpy().tobytes()[:16], dtype="<u8"))
+        if (hd, hk) != (d, k):
+            raise ValueError(f"frame header {(hd, hk)} != receiver's {(d, k)}")
+        return super().decompress(frame, out, ratio)
+
+
+def test_corrupted_frame_raises_gloo():
+    ctx = tmp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    ps = [ctx.Process(target=_corrupt_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in ps:
+        p.start()
+    res = dict(q.get(timeout=300) for _ in range(2))
+    for p in ps:
+        p.join(timeout=60)
+    assert res[1] == ["ValueError", "IndexOutOfRange"], res
 
 
 def test_frame_bytes_and_passthrough():
@@ -120,10 +178,11 @@ def test_ring_exchange_nccl_world2(cuda):
     assert res == {0: True, 1: True}, res
 
 
-def _peer_worker(rank, world, port, q, pull=False):
+def _peer_worker(rank, world, port, q, pull=False, shared=False):
     """Frames through PeerRing: push = copy engines into the successor's IPC
     buffer; pull = compress into the own exported buffer, the successor's
-    decompress reads it over NVLink.  Event handoff either way."""
+    decompress reads it over NVLink.  Event handoff either way.  `shared`: every
+    rank on cuda:0 (CUDA IPC between processes of one GPU), gloo only."""
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     try:
         import ctypes
@@ -132,10 +191,14 @@ def _peer_worker(rank, world, port, q, pull=False):
         from paper_2410_12707_b200 import _lib
         from paper_2410_12707_b200.peer import PeerRing
 
-        torch.cuda.set_device(rank)
-        dev = torch.device("cuda", rank)
-        dist.init_process_group("nccl", rank=rank, world_size=world, device_id=dev)
-        cpu = dist.new_group(backend="gloo")
+        dev = torch.device("cuda", 0 if shared else rank)
+        torch.cuda.set_device(dev)
+        if shared:
+            dist.init_process_group("gloo", rank=rank, world_size=world)
+            cpu = None
+        else:
+            dist.init_process_group("nccl", rank=rank, world_size=world, device_id=dev)
+            cpu = dist.new_group(backend="gloo")
         L = _lib.lib()
         d, r = 300_007, 50.0
         k = P.select_k(d, r)
@@ -184,14 +247,18 @@ def _peer_worker(rank, world, port, q, pull=False):
 
 
 @pytest.mark.gpu
+@pytest.mark.parametrize("shared", [False, True], ids=["2gpu", "1gpu"])
 @pytest.mark.parametrize("pull", [False, True], ids=["push", "pull"])
-def test_peer_ring_world2(cuda, pull):
-    if torch.cuda.device_count() < 2:
+def test_peer_ring_world2(cuda, pull, shared):
+    """2gpu: one rank per GPU over NVLink.  1gpu: both ranks on cuda:0 (two
+    processes, CUDA IPC on one device): the same ring code, events and frame
+    checks, runnable on a one-GPU box."""
+    if not shared and torch.cuda.device_count() < 2:
         pytest.skip("needs 2 GPUs (run under gpurun --gpus 2)")
     ctx = tmp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    ps = [ctx.Process(target=_peer_worker, args=(r, 2, port, q, pull)) for r in range(2)]
+    ps = [ctx.Process(target=_peer_worker, args=(r, 2, port, q, pull, shared)) for r in range(2)]
     for p in ps:
         p.start()
     res = dict(q.get(timeout=300) for _ in range(2))
