@@ -59,9 +59,12 @@ int gp_select_k(int64_t d, double ratio, int64_t* k_out);
  * Replaces wire_bytes, compressor.py:106-108. */
 int gp_wire_bytes(int64_t d, double ratio, int64_t* bytes_out);
 
-/* Scratch needed by gp_topk_compress for vectors of up to d elements on the
- * current device.  The workspace must be zeroed once (gp_workspace_init) and is
- * left zeroed by every successful call; one workspace per concurrent stream. */
+/* Scratch needed by gp_topk_compress for a length-d vector of `dtype`
+ * (sized by d: about 8 B per element for the candidate lists plus per-CTA
+ * regions).  A buffer serves every call whose own requirement fits in it.  Its
+ * state region (extent a function of the buffer size only) must be zeroed once
+ * with gp_workspace_init and is left zeroed by every call; one workspace per
+ * concurrent stream. */
 size_t gp_topk_workspace_bytes(int64_t d, int dtype);
 int gp_workspace_init(void* ws, size_t ws_bytes, void* stream);
 

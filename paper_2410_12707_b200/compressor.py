@@ -200,9 +200,8 @@ def _stream_handle(device: torch.device, stream=None) -> int:
 class _Workspace:
     """Per (device, stream) scratch for gp_topk_compress, zeroed once, grown on demand.
 
-    A workspace sized for d serves every call with d' <= d (include/adatopk.h),
-    so the cache keeps the largest d it was sized for and replaces the buffer
-    (zeroed anew) only when a longer vector arrives."""
+    The state region's extent depends only on the buffer size
+    (include/adatopk.h), so one buffer serves every vector that fits it."""
 
     _cache: dict = {}
 
@@ -210,15 +209,12 @@ class _Workspace:
     def get(cls, device: torch.device, stream_ptr: int, d: int, dtype_code: int) -> tuple[int, int]:
         need = int(_lib.lib().gp_topk_workspace_bytes(d, dtype_code))
         key = (device.index, stream_ptr)
-        ent = cls._cache.get(key)
-        if ent is None or ent[1] < d or ent[0].numel() < need:
-            dd = max(d, ent[1] if ent is not None else 0)
-            need = max(need, int(_lib.lib().gp_topk_workspace_bytes(dd, _lib.DTYPE_F64)))  # any dtype up to dd
+        buf = cls._cache.get(key)
+        if buf is None or buf.numel() < need:
             buf = torch.empty(need, dtype=torch.uint8, device=device)
             raise_for_status(_lib.lib().gp_workspace_init(buf.data_ptr(), need, stream_ptr), "gp_workspace_init")
-            ent = (buf, dd)
-            cls._cache[key] = ent
-        return ent[0].data_ptr(), int(ent[0].numel())
+            cls._cache[key] = buf
+        return buf.data_ptr(), int(buf.numel())
 
     @classmethod
     def clear(cls) -> None:

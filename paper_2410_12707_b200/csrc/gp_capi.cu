@@ -119,14 +119,16 @@ int gp_wire_bytes(int64_t d, double ratio, int64_t* bytes_out) {
 
 size_t gp_topk_workspace_bytes(int64_t d, int dtype) {
   if (d < 0) d = 0;
-  return gp::compress_workspace_layout((uint64_t)d, dtype, nullptr);
+  return gp::compress_workspace_bytes((uint64_t)d, dtype);
 }
 
 int gp_workspace_init(void* ws, size_t ws_bytes, void* stream) {
   if (!ws) return GP_ERR_INVALID_ARGUMENT;
-  // the whole buffer (the state regions' sizes depend on the d it was sized
-  // for); once: every call leaves the state it uses zeroed
-  return cudaMemsetAsync(ws, 0, ws_bytes, as_stream(stream)) == cudaSuccess ? GP_OK : GP_ERR_CUDA;
+  // the state region (its extent depends only on ws_bytes); once: every call
+  // leaves it zeroed again
+  size_t n = gp::workspace_state_bytes(ws_bytes);
+  if (n > ws_bytes) n = ws_bytes;
+  return cudaMemsetAsync(ws, 0, n, as_stream(stream)) == cudaSuccess ? GP_OK : GP_ERR_CUDA;
 }
 
 static int compress_impl(const void* x, int dtype, int64_t d, int64_t k, void* idx_out, int idx_bytes,
@@ -139,7 +141,7 @@ static int compress_impl(const void* x, int dtype, int64_t d, int64_t k, void* i
   if (idx_bytes != 4 && idx_bytes != 8) return GP_ERR_INVALID_ARGUMENT;
   if (val_dtype != GP_DTYPE_F32 && val_dtype != dtype) return GP_ERR_INVALID_ARGUMENT;
   gp::WsLayout l;
-  const size_t need = gp::compress_workspace_layout((uint64_t)d, dtype, &l);
+  const size_t need = gp::compress_workspace_layout((uint64_t)d, dtype, ws_bytes, &l);
   if (ws_bytes < need) return GP_ERR_INVALID_ARGUMENT;
   gp::DeviceInfo dev;
   if (device_info(&dev)) return GP_ERR_CUDA;

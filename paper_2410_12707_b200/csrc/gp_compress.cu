@@ -1307,27 +1307,35 @@ int launch_compress(int dtype, CompressArgs a, const DeviceInfo& dev, cudaStream
   }
 }
 
-// Workspace of a length-d compress, sized by d: the fine histogram by the
-// fine-bit count the launcher picks for d (f32/f64 rule for every dtype), the
-// per-CTA regions by the largest grid d can get (grid_bound), the candidate
-// lists by d.  The regions that must stay zeroed (ctrl, histograms) come
-// first and grow with d only, so a workspace sized for d and zeroed once
-// serves every later call with d' <= d: the state regions of d' lie inside
-// those of d.
-size_t compress_workspace_layout(uint64_t d, int dtype, WsLayout* out) {
+// Workspace layout.  The state that must stay zeroed between calls (control
+// words, level histograms, the fine histogram) sits at the front at offsets
+// that depend only on ws_bytes: the fine histogram is sized for the largest
+// vector any call could fit in ws_bytes (lists take >= 8 B per element, so
+// d <= ws_bytes / 8).  Every call on a buffer therefore sees the same state
+// region, whatever its d and dtype, and the per-call regions behind it (per-CTA
+// counters and final-candidate regions sized by the grid d can get, candidate
+// lists sized by d) never overlap it.
+static size_t state_bytes(size_t ws_bytes) {
+  auto up = [](size_t v) { return (v + 255) & ~(size_t)255; };
+  const size_t nfine = (size_t)1 << fine_bits_for(false, ws_bytes / 8);
+  return up(256) + up((size_t)8 * 256 * 4) + up(((size_t)(kHistCopies - 1) * kFineBinsMax + nfine) * 4);
+}
+
+size_t workspace_state_bytes(size_t ws_bytes) { return state_bytes(ws_bytes); }
+
+size_t compress_workspace_layout(uint64_t d, int dtype, size_t ws_bytes, WsLayout* out) {
   const size_t entry = dtype == 2 ? 16 : 8;
   const size_t key = dtype == 2 ? 8 : 4;
   const size_t gmax = grid_bound(d);
-  const size_t nfine = (size_t)1 << fine_bits_for(false, d);
   auto up = [](size_t v) { return (v + 255) & ~(size_t)255; };
   WsLayout l;
   size_t off = 0;
   l.ctrl = off;
   off = up(off + 256);
-  l.hist1 = off;
-  off = up(off + ((size_t)(kHistCopies - 1) * kFineBinsMax + nfine) * 4);  // replica r at r * kFineBinsMax
   l.hist_lvl = off;
   off = up(off + (size_t)8 * 256 * 4);
+  l.hist1 = off;  // replica r at r * kFineBinsMax; capacity for any d that fits ws_bytes
+  off = state_bytes(ws_bytes);
   l.cta_a = off;
   off = up(off + gmax * 4);
   l.cta_b = off;
@@ -1335,10 +1343,22 @@ size_t compress_workspace_layout(uint64_t d, int dtype, WsLayout* out) {
   l.fcreg = off;
   off = up(off + gmax * kFcCap * key);
   l.lists = off;
-  off = up(off + ((size_t)d + (size_t)gmax * 32 * 16) * entry);
+  off = up(off + ((size_t)d + gmax * 32 * 16) * entry);
   l.total = off;
   if (out) *out = l;
   return off;
+}
+
+// Smallest buffer whose layout fits a length-d compress: the fine histogram
+// grows with the buffer, so iterate to the fixed point (a few steps at most).
+size_t compress_workspace_bytes(uint64_t d, int dtype) {
+  size_t ws = compress_workspace_layout(d, dtype, 0, nullptr);
+  for (int i = 0; i < 8; ++i) {
+    const size_t need = compress_workspace_layout(d, dtype, ws, nullptr);
+    if (need <= ws) break;
+    ws = need;
+  }
+  return ws;
 }
 
 }  // namespace gp

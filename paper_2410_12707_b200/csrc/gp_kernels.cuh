@@ -80,7 +80,9 @@ struct DeviceInfo {
 };
 
 int launch_compress(int dtype, CompressArgs a, const DeviceInfo& dev, cudaStream_t stream);
-size_t compress_workspace_layout(uint64_t d, int dtype, WsLayout* out);
+size_t compress_workspace_layout(uint64_t d, int dtype, size_t ws_bytes, WsLayout* out);
+size_t compress_workspace_bytes(uint64_t d, int dtype);
+size_t workspace_state_bytes(size_t ws_bytes);
 
 struct DecompressArgs {
   const void* idx;
