@@ -6,4 +6,4 @@ timeout 1500 python -m pytest tests -m gpu -x -q -p no:cacheprovider > gpurun_ou
 if [ "$1" = "bench" ]; then
   timeout 900 python bench.py --steps 10 --warmup 3 --no-pipeline > gpurun_out/bench_quick.json 2> gpurun_out/bench_quick.err
 fi
-tail -3 gpurun_out/smoke.log gpurun_out/gputests.log
+tail -n 3 gpurun_out/smoke.log gpurun_out/gputests.log
