@@ -250,18 +250,22 @@ def des_chain_fp_time(C: list, M: list, n_b: int) -> float:
     return makespan
 
 
-def measure_link_times(shape, device, reps: int = 5) -> list:
-    """Measured dense boundary transfer time (s) of every FP link s -> s+1.
+def measure_link_times(shape, device, reps: int = 5, chain: Optional[list] = None, as_tensor: bool = False):
+    """Measured dense boundary transfer time (s) of every FP link, stage s -> s+1.
 
-    Each rank sends a dense boundary tensor to its successor while receiving
-    from its predecessor (one batched NCCL group, so the links run at once, as
-    in the pipeline); the receiver times its receive with CUDA events (median of
+    Stage s runs on rank chain[s] (identity by default).  Each rank sends a
+    dense boundary tensor to its successor stage while receiving from its
+    predecessor (one batched NCCL group, so the links run at once, as in the
+    pipeline); the receiver times its receive with CUDA events (median of
     `reps`).  An all-reduce gives every rank the same vector, so every rank
     derives the same per-link plan (both ends of a link agree on k).  This is
     R_i of Eq. 6 measured instead of the alpha-beta estimate of the reference
-    CLI (cli.py:51-59).
+    CLI (cli.py:51-59).  `as_tensor`: return the float64
+    CUDA tensor (no host copy) for an on-device plan.
     """
     rank, S = dist.get_rank(), dist.get_world_size()
+    chain = list(chain) if chain is not None else list(range(S))
+    s = chain.index(rank)
     x = torch.randn(shape, device=device)
     buf = torch.empty(shape, device=device)
     t = torch.zeros(max(S - 1, 1), dtype=torch.float64, device=device)
@@ -269,10 +273,10 @@ def measure_link_times(shape, device, reps: int = 5) -> list:
     for _ in range(reps + 1):
         dist.barrier()
         ops = []
-        if rank < S - 1:
-            ops.append(dist.P2POp(dist.isend, x, rank + 1))
-        if rank > 0:
-            ops.append(dist.P2POp(dist.irecv, buf, rank - 1))
+        if s < S - 1:
+            ops.append(dist.P2POp(dist.isend, x, chain[s + 1]))
+        if s > 0:
+            ops.append(dist.P2POp(dist.irecv, buf, chain[s - 1]))
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         a.record()
         for w in dist.batch_isend_irecv(ops):
@@ -280,11 +284,11 @@ def measure_link_times(shape, device, reps: int = 5) -> list:
         b.record()
         torch.cuda.synchronize()
         samples.append(a.elapsed_time(b) * 1e-3)
-    if rank > 0:
+    if s > 0:
         samples = sorted(samples[1:])
-        t[rank - 1] = samples[len(samples) // 2]
+        t[s - 1] = samples[len(samples) // 2]
     dist.all_reduce(t)
-    return t.tolist()
+    return t if as_tensor else t.tolist()
 
 
 def measured_link_plan(n_stages: int, ratio: float, link_times: list, boundary: int, device) -> CompressionPlan:
@@ -582,13 +586,28 @@ class DistPipeline:
 MODELS = {"small": GPT2_SMALL, "medium": GPT2_MEDIUM, "xl": GPT2_XL}
 
 
+def _stage_links(S: int) -> list:
+    return [(s, s + 1) for s in range(S - 1)] + [(s + 1, s) for s in range(S - 1)]
+
+
 def run_pipeline(model: str = "medium", plan_mode: str = "uniform", ratio: float = 100.0, micro_batch: int = None,
-                 n_micro: int = None, seq_len: int = 1024, steps: int = 3, warmup: int = 1) -> dict:
+                 n_micro: int = None, seq_len: int = 1024, steps: int = 3, warmup: int = 1, codec=None,
+                 codec_name: str = "sm_100a FrameCodec") -> dict:
     """Time GPipe steps of GPT-2 with one stage per rank (or one stage on one GPU).
 
+    plan_mode:
+      "uniform"  every FP/BP link at `ratio` (uniform_plan, compressor.py:132-139);
+      "measured" link times measured on the NVLink fabric, Eq. 6 + select_k on the
+                 device (DevicePlan): the compress kernels read k from device
+                 memory, the receivers read it from the frame headers;
+      "adatopk"  configs[3]: the reference's unchanged OP-Fence schedule over a
+                 simulated two-cluster network (opfence_plan) gives the stage ->
+                 GPU chain and the block ranges, the reference CLI's
+                 cross_link_times gives R_i (mirrored onto BP links), and Eq. 6
+                 (adatopk_plan) the per-link ratios.
     Returns samples/s = global batch / median step time (CUDA events, each step
-    the max over ranks) after `warmup` untimed steps.
-    Call after torch.distributed is initialised when WORLD_SIZE > 1.
+    the max over ranks) after `warmup` untimed steps.  Call after
+    torch.distributed is initialised when WORLD_SIZE > 1.
     """
     cfg = MODELS[model]
     mb = micro_batch or (8 if model != "xl" else 4)
@@ -596,14 +615,24 @@ def run_pipeline(model: str = "medium", plan_mode: str = "uniform", ratio: float
     n_micro = n_micro or max(4, 2 * world)
     dev = torch.device("cuda", torch.cuda.current_device())
     boundary = mb * seq_len * cfg.n_embd
-    lt = None
-    if plan_mode == "measured" and world > 1:
-        lt = measure_link_times((mb, seq_len, cfg.n_embd), dev)
-        plan = measured_link_plan(world, ratio, lt, boundary, dev)
+    lt, chain, bounds, dev_plan, plan, ofp = None, None, None, None, None, None
+    if world > 1 and plan_mode == "measured":
+        R = measure_link_times((mb, seq_len, cfg.n_embd), dev, as_tensor=True)
+        dev_plan = DevicePlan(_stage_links(world), boundary, ratio, dev)
+        dev_plan.replan(torch.cat([R, R]))  # FP time mirrored onto the BP link
+    elif world > 1 and plan_mode == "adatopk":
+        from .opfence_plan import opfence_partition
+
+        ofp = opfence_partition(cfg.n_layer, cfg.n_embd, cfg.vocab, world, mb, seq_len, n_micro)
+        chain, bounds = ofp.chain, ofp.bounds
+        plan = adatopk_plan(None, dict(ofp.link_R), ratio)
+        lt = [ofp.link_R[(s, s + 1)] for s in range(world - 1)]
+    elif world > 1:
+        plan = link_plan(world, plan_mode, ratio, None)
+    if world > 1:
+        pipe = DistPipeline(cfg, plan, mb, seq_len, chain=chain, bounds=bounds, dev_plan=dev_plan, codec=codec)
     else:
-        lt = two_cluster_link_times(world, boundary * 4) if plan_mode == "adatopk" else None
-        plan = link_plan(world, plan_mode, ratio, lt)
-    pipe = DistPipeline(cfg, plan, mb, seq_len) if world > 1 else VirtualPipeline(cfg, 1, None, dev)
+        pipe = VirtualPipeline(cfg, 1, None, dev)
     gb = mb * n_micro
     times, loss = [], float("nan")
     for i in range(warmup + steps):
@@ -623,45 +652,64 @@ def run_pipeline(model: str = "medium", plan_mode: str = "uniform", ratio: float
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         times = tt.tolist()
     t = sorted(times)[len(times) // 2]  # median step
-    model = None
-    if world > 1 and plan is not None:
-        model = _fp_model_check(pipe, cfg, plan, mb, seq_len, n_micro, ratio, dev, lt if plan_mode == "measured" else None)
     links = {}
-    if plan is not None:
+    if dev_plan is not None:
+        ks, rs = dev_plan.k.tolist(), dev_plan.r.tolist()
+        lt = [float(v) for v in R.tolist()]
+        for (s, d), k, r in zip(dev_plan.links, ks, rs):
+            links[f"{s}->{d}"] = {"ratio": round(r, 3), "k": k, "wire_bytes": 16 + 12 * k,
+                                  "frame_capacity_bytes": 16 + 12 * dev_plan.k_cap}
+    elif plan is not None:
         for (s, d), r in sorted(plan.per_link.items()):
             links[f"{s}->{d}"] = {"ratio": round(r, 3), "k": select_k(boundary, r),
                                   "wire_bytes": 16 + 12 * select_k(boundary, r)}
+    model_check = None
+    if world > 1 and (plan is not None or dev_plan is not None) and codec is None:
+        model_check = _fp_model_check(pipe, cfg, mb, seq_len, n_micro, ratio, dev,
+                                      lt if plan_mode in ("measured", "adatopk") else None, chain)
     del pipe
     torch.cuda.empty_cache()
-    return {"metric": "GPT-2 compressed-pipeline samples/s", "value": round(gb / (t * 1e-3), 3), "unit": "samples/s",
-            "n_gpus": world, "model": model, "layers": cfg.n_layer, "hidden": cfg.n_embd, "micro_batch": mb,
-            "n_micro": n_micro, "global_batch": gb, "seq_len": seq_len, "ms_per_step": round(t, 2),
-            "step_ms": [round(v, 2) for v in times], "warmup": warmup,
-            "loss": round(loss, 4), "plan": plan_mode if world > 1 else "none (1 stage, no boundary)",
-            "base_ratio": ratio, "boundary_elems": boundary, "dense_boundary_bytes": boundary * 4, "links": links,
-            "link_times_s": [round(v, 7) for v in lt] if lt is not None else None,
-            "link_times_source": {"measured": "dense boundary P2P, CUDA events, median (measure_link_times)",
-                                  "adatopk": "two-cluster alpha-beta model"}.get(plan_mode),
-            "fp_model": model,
-            "schedule": "GPipe fill-drain (executor.py:389-404), bf16 autocast, fp32 boundaries",
-            "partition": "OP-Fence FLOP-proportional contiguous split of [embeddings, blocks, head]: "
-                         + str(partition(cfg.n_layer, world, cfg)),
-            "data": "synthetic tokens, random init"}
+    out = {"metric": "GPT-2 compressed-pipeline samples/s", "value": round(gb / (t * 1e-3), 3), "unit": "samples/s",
+           "n_gpus": world, "model": model, "layers": cfg.n_layer, "hidden": cfg.n_embd, "micro_batch": mb,
+           "n_micro": n_micro, "global_batch": gb, "seq_len": seq_len, "ms_per_step": round(t, 2),
+           "step_ms": [round(v, 2) for v in times], "warmup": warmup,
+           "loss": round(loss, 4), "plan": plan_mode if world > 1 else "none (1 stage, no boundary)",
+           "codec": codec_name, "base_ratio": ratio, "boundary_elems": boundary, "dense_boundary_bytes": boundary * 4,
+           "links": links, "link_times_s": [round(v, 7) for v in lt] if lt is not None else None,
+           "link_times_source": {"measured": "dense boundary P2P, CUDA events, median (measure_link_times); "
+                                             "Eq. 6 + select_k on the device, k read by the kernels",
+                                 "adatopk": "reference cli.cross_link_times over the simulated two-cluster "
+                                            "network (alpha + beta*M per cross-device FP edge)"}.get(plan_mode),
+           "fp_model": model_check,
+           "schedule": "GPipe fill-drain (executor.py:389-404), bf16 autocast, fp32 boundaries",
+           "data": "synthetic tokens, random init"}
+    if ofp is not None:
+        out["partition"] = ("reference OP-Fence (opfence.opfence_schedule over opdag.build_dag + "
+                            "costmodel.estimate_dag_costs, baseline/_ref), blocks rounded to their add2 node")
+        out["opfence"] = ofp.to_dict()
+    else:
+        out["partition"] = ("OP-Fence FLOP-proportional contiguous split of [embeddings, blocks, head]: "
+                            + str(partition(cfg.n_layer, world, cfg)))
+    return out
 
 
-def _fp_model_check(pipe, cfg, plan, mb, seq_len, n_micro, ratio, dev, link_times=None) -> dict:
+def _fp_model_check(pipe, cfg, mb, seq_len, n_micro, ratio, dev, link_times=None, chain=None) -> dict:
     """The FP (fill) phase measured next to the planner's closed forms, from measured inputs:
     C_d = each stage's forward time for one micro-batch, R_d = the dense boundary
     receive time of the link into stage d (R_0 = 0), r_d = the plan's ratio on that link."""
-    world, rank = dist.get_world_size(), dist.get_rank()
+    world = dist.get_world_size()
     tok, tgt = synthetic_batch(cfg, mb * n_micro, seq_len, dev, seed=123)
     c = torch.zeros(world, dtype=torch.float64, device=dev)
-    c[rank] = pipe.stage_fp_time(tok, tgt)
+    c[pipe.s] = pipe.stage_fp_time(tok, tgt)  # indexed by stage
     dist.all_reduce(c)
     C = c.tolist()
-    lt = link_times if link_times is not None else measure_link_times((mb, seq_len, cfg.n_embd), dev)
+    lt = link_times if link_times is not None else measure_link_times((mb, seq_len, cfg.n_embd), dev, chain=chain)
     R = [0.0] + list(lt)
-    r_dev = [1.0] + [plan.ratio_for(s, s + 1) for s in range(world - 1)]
+    if pipe.dev_plan is not None:
+        rr = pipe.dev_plan.r.tolist()
+        r_dev = [1.0] + [rr[pipe.dev_plan.index[(s, s + 1)]] for s in range(world - 1)]
+    else:
+        r_dev = [1.0] + [pipe.plan.ratio_for(s, s + 1) for s in range(world - 1)]
 
     def timed_fp(p) -> float:
         ts = []
@@ -683,10 +731,10 @@ def _fp_model_check(pipe, cfg, plan, mb, seq_len, n_micro, ratio, dev, link_time
     d_b = mb * seq_len * cfg.n_embd
     M_comp = [0.0] + [x * (12 * select_k(d_b, q) / (4 * d_b)) if q > 1.0 else x for x, q in zip(R[1:], r_dev[1:])]
     t_comp = timed_fp(pipe)
-    saved = pipe.plan
-    pipe.plan = None  # the same stages with dense boundaries
+    saved = pipe.plan, pipe.dev_plan
+    pipe.plan, pipe.dev_plan = None, None  # the same stages with dense boundaries
     t_dense = timed_fp(pipe)
-    pipe.plan = saved
+    pipe.plan, pipe.dev_plan = saved
     return {"C_stage_fp_s": [round(v, 6) for v in C], "R_link_dense_s": [round(v, 7) for v in R],
             "r_link": [round(v, 3) for v in r_dev], "n_b": n_micro,
             "eq3_dense_fp_ms": round(1e3 * eq3_pipeline_time(C, R, n_micro), 3),
@@ -708,6 +756,7 @@ def synthetic_batch(cfg: GPT2Config, batch: int, seq_len: int, device, seed: int
 
 
 __all__ = ["GPT2Config", "GPT2_SMALL", "GPT2_MEDIUM", "GPT2_XL", "GPT2_TINY", "partition", "proportional_split", "op_flops", "make_stage",
-           "link_plan", "two_cluster_link_times", "measure_link_times", "measured_link_plan", "eq3_pipeline_time",
+           "link_plan", "two_cluster_link_times", "measure_link_times", "measured_link_plan", "DevicePlan",
+           "eq3_pipeline_time",
            "eq7_pipeline_time", "des_chain_fp_time", "VirtualPipeline", "DistPipeline", "synthetic_batch", "run_pipeline",
            ]
