@@ -1047,7 +1047,7 @@ def main():
             print(json.dumps(line), flush=True)
         return
     if world > 1:
-        os.environ.setdefault("NCCL_DEBUG", "WARN")  # keep stdout to the one JSON line
+        os.environ.pop("NCCL_DEBUG", None)  # NCCL prints a version banner whenever NCCL_DEBUG is set: stdout stays the one JSON line
         import torch
         import torch.distributed as dist
 

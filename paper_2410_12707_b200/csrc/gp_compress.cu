@@ -555,21 +555,38 @@ __global__ void __launch_bounds__(kCompressThreads, 1) compress_kernel(const Com
     // scan, so a warp's per-row dependent chain (scan, append, histogram) is
     // paid once per two rows.  Lane holds 16-byte piece h*32+lane of each row,
     // i.e. elements [h*32*EPS + lane*EPS, +EPS).
-    auto process2 = [&](uint32_t r, uint32_t so0, uint32_t so1) {
+    // FULL (both rows complete: no per-piece bounds) and ALL (every element a
+    // candidate) are compile-time in the hot loop: a full step is four
+    // back-to-back 16-byte smem loads, then one compare and one predicated OR
+    // per element, with no branch.
+    auto process2 = [&](uint32_t r, uint32_t so0, uint32_t so1, auto full_c, auto all_c) {
+      constexpr bool FULL = decltype(full_c)::value;
+      constexpr bool ALL = decltype(all_c)::value;
       uint32_t m[4];
-      const bool full = (r + 2u) * 32u <= nch;  // both rows complete: no per-piece bounds
+      if constexpr (FULL) {
+        uint4 v[4];
 #pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        const uint32_t rr = r + (j >> 1);
-        const uint32_t piece = (j & 1) * 32u + lane;
-        uint32_t mm = 0;
-        if (full || (rr < nrow && piece < 2u * min(32u, nch - rr * 32u))) {
-          const uint4 v = ld_shared_v4((j < 2 ? so0 : so1) + piece * 16u);
+        for (int j = 0; j < 4; ++j) v[j] = ld_shared_v4((j < 2 ? so0 : so1) + ((j & 1) * 32u + lane) * 16u);
 #pragma unroll
-          for (int e = 0; e < EPS; ++e)
-            if (all || test(Tr::lane(v, e))) mm |= 1u << e;
+        for (int j = 0; j < 4; ++j) {
+          uint32_t mm = 0;
+#pragma unroll
+          for (int e = 0; e < EPS; ++e) mm |= (ALL || test(Tr::lane(v[j], e))) ? (1u << e) : 0u;
+          m[j] = mm;
         }
-        m[j] = mm;
+      } else {
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const uint32_t rr = r + (j >> 1);
+          const uint32_t piece = (j & 1) * 32u + lane;
+          uint32_t mm = 0;
+          if (rr < nrow && piece < 2u * min(32u, nch - rr * 32u)) {
+            const uint4 v = ld_shared_v4((j < 2 ? so0 : so1) + piece * 16u);
+#pragma unroll
+            for (int e = 0; e < EPS; ++e) mm |= (ALL || test(Tr::lane(v, e))) ? (1u << e) : 0u;
+          }
+          m[j] = mm;
+        }
       }
       // per-sub-row counts packed into one scan: 8-bit fields when a sub-row
       // holds at most 32*EPS <= 128 candidates (f32, f64), else 16-bit fields
@@ -648,16 +665,22 @@ __global__ void __launch_bounds__(kCompressThreads, 1) compress_kernel(const Com
       fence_proxy_async_smem();
       for (uint32_t p = 0; p < min(npair, kPairs); ++p) issue(p, q0 + p);
     }
-    for (uint32_t p = 0; p < npair; ++p) {
-      const uint32_t q = q0 + p, slot = q % kPairs;
-      mbar_wait(mbar + slot * 8u, (q / kPairs) & 1u);
-      process2(2u * p, ring + slot * 2048u, ring + slot * 2048u + 1024u);
-      __syncwarp();
-      if (lane == 0 && p + kPairs < npair) {  // refill the slot just consumed
-        fence_proxy_async_smem();
-        issue(p + kPairs, q + kPairs);
+    auto run_pairs = [&](auto all_c) {
+      const uint32_t nfull = nch / 64u;  // row pairs with both rows complete
+      for (uint32_t p = 0; p < npair; ++p) {
+        const uint32_t q = q0 + p, slot = q % kPairs;
+        mbar_wait(mbar + slot * 8u, (q / kPairs) & 1u);
+        if (p < nfull) process2(2u * p, ring + slot * 2048u, ring + slot * 2048u + 1024u, std::true_type{}, all_c);
+        else process2(2u * p, ring + slot * 2048u, ring + slot * 2048u + 1024u, std::false_type{}, all_c);
+        __syncwarp();
+        if (lane == 0 && p + kPairs < npair) {  // refill the slot just consumed
+          fence_proxy_async_smem();
+          issue(p + kPairs, q + kPairs);
+        }
       }
-    }
+    };
+    if (all) run_pairs(std::true_type{});
+    else run_pairs(std::false_type{});
     seq = q0 + npair;
     const Key span = lo ? Tr::kInfAbs - lo_m1 : ~(Key)0;
     for (uint32_t i0 = nch * EPL; i0 < n; i0 += 32u) {  // scalar tail / unaligned input
