@@ -7,11 +7,31 @@
 //     key = isnan(x) ? 0 : (bits(x) & ~sign) + 1
 #pragma once
 #include <cstdint>
+#include <cstdio>
 #include <cuda_runtime.h>
 
 namespace gp {
 
 constexpr uint32_t kFull = 0xFFFFFFFFu;
+
+// Checked build (-DGP_CHECKED, the `checked` library variant): device-side
+// bounds and invariant checks that trap with the failing condition -- the
+// stand-in for compute-sanitizer, which this GPU pool does not allow.  No-ops
+// in the product build.
+#ifdef GP_CHECKED
+#define GP_CHECK(c)                                                                        \
+  do {                                                                                     \
+    if (!(c)) {                                                                            \
+      printf("GP_CHECK failed %s:%d block %d thread %d: %s\n", __FILE__, __LINE__,         \
+             (int)blockIdx.x, (int)threadIdx.x, #c);                                       \
+      __trap();                                                                            \
+    }                                                                                      \
+  } while (0)
+#else
+#define GP_CHECK(c) \
+  do {              \
+  } while (0)
+#endif
 
 // ---------------------------------------------------------------------------
 // dtype traits.  `Bits` is the raw element bit pattern, `Key` the rank key.

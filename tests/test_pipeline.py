@@ -78,6 +78,37 @@ def test_virtual_pipeline_loss_parity_vs_oracle_codec(cuda):
 
 
 @pytest.mark.gpu
+@pytest.mark.parametrize("model", ["small", "medium"])
+def test_gpt2_loss_parity_10_steps_vs_oracle_codec(cuda, model):
+    """north_star: end-to-end losses with the sm_100a codec at the boundaries
+    match a run with the CPU reference compressor (the oracle, host round trip)
+    within rel 1e-3 over 10 steps, at GPT-2 small (12 x 768) and medium (24 x
+    1024) widths, 2 stages, r = 100 (sequence 128, so the CPU codec stays fast)."""
+    cfg = {"small": PL.GPT2_SMALL, "medium": PL.GPT2_MEDIUM}[model]
+    plan = PL.link_plan(2, "uniform", 100.0)
+
+    def run(codec):
+        torch.manual_seed(0)
+        pipe = PL.VirtualPipeline(cfg, 2, plan, cuda, codec=codec, lr=1e-4, seed=7, sdpa=False)
+        out = []
+        for i in range(10):
+            tok, tgt = PL.synthetic_batch(cfg, 4, 128, cuda, seed=100 + i)
+            out.append(pipe.step(tok, tgt, n_micro=4))
+        return out, pipe.stats
+
+    torch.use_deterministic_algorithms(True, warn_only=True)
+    try:
+        gpu, st = run(None)
+        ref, _ = run(OracleCodec())
+    finally:
+        torch.use_deterministic_algorithms(False)
+    assert st.compress_calls == 10 * 4 * 2
+    for a, b in zip(gpu, ref):
+        assert abs(a - b) <= REL_TOL * abs(b), (gpu, ref)
+    assert gpu[-1] < gpu[0]
+
+
+@pytest.mark.gpu
 def test_compressed_pipeline_trains(cuda):
     losses, st = _losses(None, cuda, steps=12, plan_ratio=4.0)
     assert losses[-1] < losses[0]
