@@ -657,6 +657,11 @@ def run_ours(args, rank, world, local_rank):
                               "note": "int32 indices + f32 values (8 B/elem), algorithmic bytes d*4 + 8k per launch"}
     if rank == 0 and world == 1:
         line["c1_gpt2_small"] = bench_c1(P, L, dev, flush, peak)
+        if not args.no_sweep:
+            try:
+                line["sweep_configs4"] = bench_sweep(L, dev, flush, peak)
+            except Exception as exc:  # noqa: BLE001  (informative sub-object)
+                line["sweep_configs4"] = {"error": f"{type(exc).__name__}: {exc}"[:300]}
         line["cpu_baseline"] = cpu_baseline()
         line["e2e"] = bench_e2e(P, dev)
         line["gpu_comparator_torch_topk"] = bench_torch_topk(units, dev, flush)
@@ -916,6 +921,67 @@ def gpt2_batch(L, dev, shape, n, ns, flush, ratio=100.0, reps=10):
     return t, n * pair_bytes(d, 4, k) / (t * 1e-6) / 1e9
 
 
+def bench_sweep(L, dev, flush, peak):
+    """configs[4] on the GPU: {1, 4, 16, 64, 256, 1024} MB x r = 10..10^4 x fp32/bf16,
+    one tensor per launch, compress and decompress device times from CUDA graphs
+    after a 512 MB L2 flush (scripts/sweep.py's method), every result checked by
+    size-independent properties (k, strictly increasing indices, threshold
+    separation, tie order, round trip).  The CPU reference leg of the same sweep
+    (minutes of single-core argsort) is in profiles/sweep_r02.json."""
+    import torch
+
+    from scripts.graph_timing import graph_time
+    from scripts.sweep import RATIOS as SR, SIZES_MB, check
+
+    rows = []
+    for dt, code, esz in (("fp32", 0, 4), ("bf16", 1, 2)):
+        for mb in SIZES_MB:
+            d = (mb << 20) // esz
+            g = torch.Generator(device=dev).manual_seed(mb)
+            x = torch.randn(d, device=dev, generator=g)
+            if dt == "bf16":
+                x = x.to(torch.bfloat16)
+            wsb = L.gp_topk_workspace_bytes(d, code)
+            ws = torch.empty(wsb, dtype=torch.uint8, device=dev)
+            sp = torch.cuda.current_stream().cuda_stream
+            L.gp_workspace_init(ws.data_ptr(), wsb, sp)
+            out = torch.empty(d, dtype=x.dtype, device=dev)
+            err = torch.zeros(1, dtype=torch.int32, device=dev)
+            for r in SR:
+                k = select_k(d, r)
+                frame = torch.empty(16 + 12 * k, dtype=torch.uint8, device=dev)
+
+                def fl():
+                    flush.sum()
+
+                def comp():
+                    assert L.gp_topk_compress_frame(x.data_ptr(), code, d, k, frame.data_ptr(), ws.data_ptr(), wsb,
+                                                    torch.cuda.current_stream().cuda_stream) == 0
+
+                def dec():
+                    assert L.gp_topk_decompress_frame(frame.data_ptr(), k, d, out.data_ptr(), code, 0, err.data_ptr(),
+                                                      torch.cuda.current_stream().cuda_stream) == 0
+
+                n = 3 if mb >= 256 else 6
+                t0 = graph_time([fl], n=n, reps=2)
+                tc = graph_time([fl, comp], n=n, reps=2) - t0
+                td = graph_time([fl, comp, dec], n=n, reps=2) - (tc + t0)
+                torch.cuda.synchronize()
+                comp()
+                dec()
+                torch.cuda.synchronize()
+                assert int(err.item()) == 0
+                check(x, frame, k, d, out)
+                alg = d * esz + 12 * k
+                rows.append([dt, mb, r, round(tc, 1), round(td, 1), round(2 * alg / (tc + td) / 1e3 / peak, 3)])
+            del x, ws, out, frame
+            torch.cuda.empty_cache()
+    return {"columns": ["dtype", "size_mb", "ratio", "compress_us", "decompress_us", "pair_frac_of_peak"],
+            "rows": rows, "checked": "every row: k, strictly increasing indices, threshold separation, tie order, "
+                                     "round trip (scripts/sweep.py check)",
+            "timing": "CUDA graphs, each launch after a 512 MB L2 read flush, differenced; algorithmic bytes d*s+12k"}
+
+
 def bench_torch_topk(units, dev, flush, reps=3):
     """Informative GPU comparator (the paper's), not a parity path:
     per pair torch.topk(|x|, k, sorted=False) + index sort + value gather, then a zeroed output and
@@ -1037,6 +1103,7 @@ def main():
                          "the compress kernel's own stores there, or NCCL batch_isend_irecv")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-pipeline", action="store_true", help="skip the GPT-2 pipeline sub-measurement")
+    ap.add_argument("--no-sweep", action="store_true", help="skip the configs[4] GPU sweep sub-measurement")
     args = ap.parse_args()
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
