@@ -719,9 +719,8 @@ __global__ void __launch_bounds__(kCompressThreads, 1) compress_kernel(const Com
   // and find the fine bin holding the k-th largest key
   uint32_t B1 = 0, G1 = 0, M = 0;
   uint32_t pop_lo = 0, pop_hi = 0;  // every populated bin of every replica lies in [pop_lo, pop_hi)
-  auto find_b1 = [&]() -> bool {
-    const uint32_t mb = ctrl[kCtrlMaxBin];
-    const int lowest = (int)(0xFFFFFFFFu - ctrl[kCtrlMinLoBin]);  // no bin below any watermark is populated
+  auto find_b1 = [&](uint32_t mb, uint32_t minlo_c) -> bool {
+    const int lowest = (int)(0xFFFFFFFFu - minlo_c);  // no bin below any watermark is populated
     pop_lo = (uint32_t)lowest;
     pop_hi = mb;
     if (tid == 0) sh_res[0] = 0u;
@@ -781,8 +780,12 @@ __global__ void __launch_bounds__(kCompressThreads, 1) compress_kernel(const Com
       grid_barrier(bar, G);  // ---- B1 (and the rescan barrier)
       if (pass == 0) STAMP(3);
       EXIT_AT(3);
-      const bool found = (pass == 1 || ctrl[kCtrlCands] >= k) && find_b1();
-      if (pass == 1 || (found && ctrl[kCtrlMaxLoBin] - 1u <= B1)) break;
+      // every control word in one round trip (four independent loads), not
+      // one dependent L2 trip per decision
+      const uint32_t c_mb = ctrl[kCtrlMaxBin], c_maxlo = ctrl[kCtrlMaxLoBin], c_cands = ctrl[kCtrlCands],
+                     c_minlo = ctrl[kCtrlMinLoBin];
+      const bool found = (pass == 1 || c_cands >= k) && find_b1(c_mb, c_minlo);
+      if (pass == 1 || (found && c_maxlo - 1u <= B1)) break;
       lo = (Key)(found ? B1 : 0u) << FS;
       add_below = my_lobin;
     }
@@ -1262,10 +1265,13 @@ __global__ void __launch_bounds__(256) keep_all_kernel(const CompressArgs a) {
 
 // Fine-histogram resolution: 16 bits up to 2^23 elements, +1 bit per doubling
 // (max 20), so the population of the threshold bin stays roughly constant.
+#ifndef GP_FB_SHIFT
+#define GP_FB_SHIFT 5
+#endif
 static int fine_bits_for(bool direct_t, uint64_t d) {
   if (direct_t) return 16;
   int fb = 16;
-  while (fb < kFineBitsMax && (d >> (fb + 7)) != 0) ++fb;
+  while (fb < kFineBitsMax && (d >> (fb + GP_FB_SHIFT)) != 0) ++fb;
   return fb;
 }
 template <class Tr>
