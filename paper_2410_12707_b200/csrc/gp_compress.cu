@@ -41,7 +41,9 @@
 //            the low bits with global per-level histograms + barriers, then
 //            one more barrier for the tie prefix.
 //
-// fb (fine-histogram bits) grows with d so |B1| stays small for large tensors.
+// fb (fine-histogram bits) grows with d so |B1| stays small: 16 bits below 2^21
+// elements, one more per doubling, at most 20 (GP_FB_SHIFT 5; against 7 on a
+// B200 A/B: 26 MB compresses at r = 10 -8%, the bench +0.7%).
 // All histogram state is left zeroed for the next call and the grid barrier
 // is self-resetting, so the workspace needs to be zeroed only once.
 #include <algorithm>
