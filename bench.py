@@ -504,7 +504,10 @@ def run_ours(args, rank, world, local_rank):
     t_one = torch.tensor([time.perf_counter() - t_one], device=dev)
     if world > 1:
         dist.all_reduce(t_one, op=dist.ReduceOp.MAX)
-    for _ in range(max(1, min(400, int(0.8 / max(float(t_one.item()), 1e-4))))):
+    n_spin = max(1, min(400, int(0.8 / max(float(t_one.item()), 1e-4))))
+    if os.environ.get("GP_BENCH_SPINUP") is not None:  # development aid (ncu runs): a fixed spin-up count
+        n_spin = int(os.environ["GP_BENCH_SPINUP"])
+    for _ in range(n_spin):
         step()
     torch.cuda.synchronize(dev)
     for _ in range(args.warmup):

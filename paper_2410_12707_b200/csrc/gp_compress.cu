@@ -65,6 +65,14 @@ constexpr uint32_t kFcCapBig = 65536;  // final candidates the fast path accepts
 #ifndef GP_DEFER_REST
 #define GP_DEFER_REST 1
 #endif
+#ifndef GP_WM_REFINE
+#define GP_WM_REFINE 1
+#endif
+constexpr int kWmFineBins = 4096;      // watermark refinement: fine sample bins (in the window's smem)
+#ifndef GP_REFINE_MIN_ROWS
+#define GP_REFINE_MIN_ROWS 32
+#endif
+constexpr size_t kRefineMinUnitBytes = (size_t)GP_REFINE_MIN_ROWS * 1024;  // refine for units of >= this many rows
 #ifndef GP_PREFETCH_ROWS
 #define GP_PREFETCH_ROWS 8
 #endif
@@ -331,7 +339,7 @@ struct Smem {
 // ---------------------------------------------------------------------------
 // the kernel
 
-template <class Tr>
+template <class Tr, bool kRefine>
 __global__ void __launch_bounds__(kCompressThreads, 1) compress_kernel(const CompressArgs a) {
   using Bits = typename Tr::Bits;
   using Key = typename Tr::Key;
@@ -444,7 +452,14 @@ __global__ void __launch_bounds__(kCompressThreads, 1) compress_kernel(const Com
 
   // ---- stage 0: low watermark from a sample of this CTA's row 0s (no extra
   // traffic): 4 elements per lane, one warp finds the crossing from the top
+  // Watermark refinement (below) for large units only (>= GP_REFINE_MIN_ROWS
+  // rows per warp: the bench's capped grids, GPT-2 tensors in flight): its
+  // ~2 us of prologue outweigh the candidates it saves on smaller units (A/B
+  // on B200: 21-row units +1-3 us, 43-row neutral, 87-row and longer -4..-9%).
+  constexpr bool refine = GP_WM_REFINE && kRefine;  // the launcher picks the instantiation by unit size
   for (uint32_t i = tid; i < kCoarseBins; i += kCompressThreads) sh_coarse[i] = 0u;
+  if (refine)  // the refinement's fine sample bins (the window, free until the stream)
+    for (uint32_t i = tid; i < kWmFineBins; i += kCompressThreads) sh_win[i] = 0u;
   if (tid < 32) sh_res[tid] = 0u;
   __syncthreads();
   if (nrow > 0) {
@@ -487,7 +502,68 @@ __global__ void __launch_bounds__(kCompressThreads, 1) compress_kernel(const Com
     }
   }
   __syncthreads();
-  const Key lo0 = sh_res[17] ? (Key)(sh_res[17] - 1) << CS : (Key)0;
+  Key lo0 = sh_res[17] ? (Key)(sh_res[17] - 1) << CS : (Key)0;
+  // refinement: the coarse watermark above sits on a 12-bit bin edge from 4
+  // keys per lane, so its margin and its rounding let through up to ~5x k
+  // candidates (r = 1000).  Every key of row pair 0 (16 per lane for fp32) at
+  // or above it goes into 4096 sample bins 8 key bits finer, and the
+  // watermark moves up to the fine bin where the expected population of the
+  // larger sample, plus the same 4-sigma+8 margin, is reached.  It only ever
+  // rises, and a watermark above the threshold is still caught by the rescan.
+  if (refine && sh_res[17] != 0u) {
+    constexpr int RS = CS - 8;
+    const Key la = lo0;
+    if (nrow > 0) {
+      uint32_t ns = 0, na = 0;
+      const uint32_t npc = 2u * min(nch, 64u);  // 16-byte pieces of row pair 0
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const uint32_t piece = q * 32u + lane;
+        if (piece < npc) {
+          const uint4 v = ld_shared_v4(ring + piece * 16u);
+#pragma unroll
+          for (int e = 0; e < EPS; ++e) {
+            const Key kk = Tr::key(Tr::lane(v, e));
+            if (kk >= la) {
+              const Key off = (kk - la) >> RS;
+              atomicAdd(&sh_win[off < (Key)(kWmFineBins - 1) ? (uint32_t)off : (uint32_t)(kWmFineBins - 1)], 1u);
+              ++na;
+            }
+          }
+          ns += EPS;
+        }
+      }
+      ns = warp_sum(ns);
+      na = warp_sum(na);
+      if (lane == 0 && ns) {
+        atomicAdd(&sh_res[23], ns);
+        atomicAdd(&sh_res[22], na);
+      }
+    }
+    __syncthreads();
+    const double mu2 = (double)sh_res[23] * (double)k / (double)d;
+    const double rs2 = ceil(mu2 + 4.0 * sqrt(mu2) + 8.0);
+    if (rs2 <= (double)sh_res[22]) {  // CTA-uniform
+      static_assert(kWmFineBins == 4 * kCompressThreads, "one block scan over the fine sample bins");
+      uint32_t v[4], sum = 0;
+#pragma unroll
+      for (int b = 0; b < 4; ++b) {  // thread order = descending bins
+        v[b] = sh_win[kWmFineBins - 1 - 4 * tid - b];
+        sum += v[b];
+      }
+      uint32_t tot;
+      uint32_t run = block_excl_scan(sum, sh32, &tot);  // sample keys in higher bins
+#pragma unroll
+      for (int b = 0; b < 4; ++b) {
+        if ((double)run < rs2 && (double)(run + v[b]) >= rs2) sh_res[21] = kWmFineBins - 4 * tid - b;  // bin + 1
+        run += v[b];
+      }
+      __syncthreads();
+      // down to a fine-histogram bin edge: a CTA must count every key of its
+      // lowest histogram bin, or the threshold bin's population is short
+      if (sh_res[21] != 0u) lo0 = ((la + ((Key)(sh_res[21] - 1u) << RS)) >> FS) << FS;
+    }
+  }
   const uint32_t cmax = sh_res[16] ? sh_res[16] - 1 : (uint32_t)(kCoarseBins - 1);  // highest sampled coarse bin
   // top of the smem histogram window: two exponents above the sample maximum
   const uint32_t top = min(nfine, ((cmax + 1u) << (FB - 12)) + (2u << (FB - Tr::kExpBits)));
@@ -1294,18 +1370,26 @@ static int launch_compress_t(CompressArgs a, const DeviceInfo& dev, cudaStream_t
     keep_all_kernel<Tr><<<blocks, 256, 0, stream>>>(a);
     return cudaGetLastError() == cudaSuccess ? 0 : 5;
   }
-  // per-device: the kernel's smem attribute set once and its occupancy (0 =
+  // per-device: the kernels' smem attribute set once and their occupancy (0 =
   // not yet known); concurrent first calls do the same idempotent setup
   static std::atomic<int> blocks_per_sm[kMaxDevices];
   const size_t smem = Smem<Tr>::total;
   if (dev.ordinal < 0 || dev.ordinal >= kMaxDevices) return 5;
   int nb = blocks_per_sm[dev.ordinal].load(std::memory_order_acquire);
   if (!nb) {
-    if (cudaFuncSetAttribute(compress_kernel<Tr>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+    if (cudaFuncSetAttribute(compress_kernel<Tr, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
+            cudaSuccess ||
+        cudaFuncSetAttribute(compress_kernel<Tr, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
+            cudaSuccess)
       return 5;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, compress_kernel<Tr>, kCompressThreads, smem) != cudaSuccess ||
-        nb < 1)
+    int nb2 = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, compress_kernel<Tr, false>, kCompressThreads, smem) !=
+            cudaSuccess ||
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb2, compress_kernel<Tr, true>, kCompressThreads, smem) !=
+            cudaSuccess)
       return 5;
+    nb = std::min(nb, nb2);
+    if (nb < 1) return 5;
     blocks_per_sm[dev.ordinal].store(nb, std::memory_order_release);
   }
   uint32_t gmax = (uint32_t)std::min(dev.num_sms * nb, kMaxGridSpec);
@@ -1326,7 +1410,11 @@ static int launch_compress_t(CompressArgs a, const DeviceInfo& dev, cudaStream_t
   attr[0].val.cooperative = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, compress_kernel<Tr>, a) == cudaSuccess ? 0 : 5;
+  // watermark refinement for units of >= GP_REFINE_MIN_ROWS rows (see the kernel)
+  const bool refine = (size_t)a.W * sizeof(typename Tr::Elem) >= kRefineMinUnitBytes;
+  const cudaError_t e = refine ? cudaLaunchKernelEx(&cfg, compress_kernel<Tr, true>, a)
+                               : cudaLaunchKernelEx(&cfg, compress_kernel<Tr, false>, a);
+  return e == cudaSuccess ? 0 : 5;
 }
 
 int launch_compress(int dtype, CompressArgs a, const DeviceInfo& dev, cudaStream_t stream) {
