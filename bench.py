@@ -7,25 +7,27 @@ Workload (BASELINE.json configs[1]): ResNet-101 batch-64 stage-boundary tensors
 at 224^2 — [64,256,56,56], [64,512,28,28], [64,1024,14,14], [64,2048,7,7] —
 each as an activation (ReLU(N(0,1))) and a gradient (N(0,1)*1e-3), fp32, at
 keep ratios 0.1 / 0.01 / 0.001 (r = 10 / 100 / 1000): 24 compress+decompress
-pairs per step, 771 MB of dense input per step.  Synthetic data, seeded.
+pairs per step on 24 distinct inputs (2.3 GB per step).  Synthetic data, seeded.
 
 One step = every pair through the sm_100a kernels.  At N > 1 (torchrun, one
-process per GPU, NCCL) every rank runs the same workload (weak scaling) and
-the step includes the path's exchange: each rank's compressed frames go to
-rank+1 and the frames from rank-1 are decompressed — the compressed
-stage-boundary send/recv of the north star.  `value` is algorithmic bytes of
-the whole job per second of the slowest rank (CUDA events, max over ranks).
-Algorithmic bytes per pair: compress d*4 + 12k, decompress
-12k + d*4.
+process per GPU) every rank runs the same workload (weak scaling) and the step
+includes the path's exchange: each rank's compressed frames go to rank+1 (copy
+engines over NVLink into the successor's CUDA-IPC buffer, or NCCL P2P) and the
+frames from rank-1 are decompressed — the compressed stage-boundary send/recv of
+the north star.  `value` is algorithmic bytes of the whole job per second of
+the slowest rank (CUDA events, max over ranks).  Algorithmic bytes per pair
+(SURVEY.md §8d): compress d*4 + 12k, decompress 12k + d*4.
 
-`--impl reference` times the reference algorithm on the host (the NumPy port
-in oracle/, the reference being pure Python + NumPy) on a bounded sample of
-the same workload, rank 0 only.
+`--impl reference` times the reference's own compressor (geopipe.compressor,
+the offline install in baseline/_ref; the oracle's NumPy port where it is
+absent) on the identical workload, every host core, rank 0 only; both arms
+report the same `config`.
 """
 from __future__ import annotations
 
 import argparse
 import json
+import math
 import multiprocessing as mp
 import os
 import statistics
@@ -45,6 +47,16 @@ C3_SHAPE = (8, 1024, 1024)  # GPT-2 medium boundary (configs[2])
 METRIC = "AdaTopK compress+decompress GB/s"
 WORKLOAD = ("configs[1]: ResNet-101 batch-64 stage-boundary activation+gradient compression, "
             "keep ratios 0.1/0.01/0.001, fp32, 224x224 boundaries")
+
+
+def workload_config():
+    """The `config` both arms report, identical by construction: the workload, not how an arm runs it."""
+    return {"workload": WORKLOAD, "shapes": [list(s) for s in SHAPES], "ratios": RATIOS,
+            "pairs_per_step": len(SHAPES) * len(KINDS) * len(RATIOS),
+            "bytes_per_step_per_rank": sum(pair_bytes(math.prod(sh), 4, select_k(math.prod(sh), r))
+                                           for sh in SHAPES for _ in KINDS for r in RATIOS),
+            "inputs": "24 distinct fp32 tensors per step (2.3 GB), seeded ReLU(N(0,1)) activations and "
+                      "N(0,1)*1e-3 gradients"}
 
 
 def select_k(d, r):
@@ -162,17 +174,24 @@ def run_reference(args, rank, world):
                 jobs.append((shm.name, x.size, r))
     jobs.sort(key=lambda j: -j[1])  # longest first
     cores = min(len(jobs), ncpu)
-    n_warm, n_steps = min(args.warmup, 1), max(1, min(args.steps, 3))
+    n_warm, n_steps = args.warmup, max(1, args.steps)
+    budget_s = float(os.environ.get("GP_REF_BUDGET_S", "900"))  # the whole arm stays within a few minutes
     times, nbytes = [], 0
     try:
         with mp.get_context("spawn").Pool(cores) as pool:
-            for step in range(n_warm + n_steps):
+            step = 0
+            while step < n_warm + n_steps:
                 t0 = time.perf_counter()
                 res = pool.map(_ref_job, jobs, chunksize=1)
                 dt = time.perf_counter() - t0
+                if step == 0 and dt * (n_warm + n_steps) > budget_s:
+                    # a slow host: shrink the run to fit the budget, reported in the line
+                    n_steps = max(1, int(budget_s / dt) - 1)
+                    n_warm = min(n_warm, 1)
                 if step >= n_warm:
                     times.append(dt)
                     nbytes = sum(res)
+                step += 1
     finally:
         for shm in shms:
             shm.close()
@@ -181,15 +200,15 @@ def run_reference(args, rank, world):
     value = nbytes / t / 1e9
     _, ckind, cname = _cpu_impl()
     desc = (f"the full configs[1] workload per step: {len(jobs)} compress+decompress pairs (24 distinct fp32 "
-            f"inputs, 2.3 GB), {cname}, process pool over {cores} of {ncpu} host cores, longest pairs first; "
-            f"capped at {n_warm} warm-up + {n_steps} timed steps (~20 s each)")
+            f"inputs, 2.3 GB, generated once into shared memory), {cname}, process pool over {cores} of {ncpu} "
+            f"host cores, longest pairs first")
     return {
         "impl": "reference", "metric": METRIC, "value": round(value, 4), "unit": "GB/s", "n_gpus": world,
-        "steps": n_steps, "warmup": n_warm, "steps_requested": args.steps, "warmup_requested": args.warmup,
+        "steps": n_steps, "warmup": n_warm,
         "ms_per_step": round(1e3 * t, 2), "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": "f32", "data": "synthetic (seeded ReLU(N(0,1)) activations, N(0,1)*1e-3 gradients)",
-        "config": {"workload": WORKLOAD, "shapes": [list(s) for s in SHAPES], "ratios": RATIOS,
-                   "pairs_per_step": len(jobs), "bytes_per_step": nbytes, "sample": desc, "same_as_gpu_arm": True},
+        "config": workload_config(),
+        "method": {"arm": desc, "bytes_per_step_measured": nbytes},
         "cpu_baseline": {"value": round(value, 4), "unit": "GB/s", "cores": cores, "kind": ckind, "sample": desc,
                          "cpu_count": ncpu, "cpu_model": _cpu_model()},
         "e2e": {"value": round(value, 4), "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -581,8 +600,8 @@ def run_ours(args, rank, world, local_rank):
         "warmup": args.warmup, "ms_per_step": round(t_step, 4), "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f32",
         "data": "synthetic (seeded ReLU(N(0,1)) activations, N(0,1)*1e-3 gradients, per-rank seeds)",
-        "config": {"workload": WORKLOAD, "shapes": [list(s) for s in SHAPES], "ratios": RATIOS,
-                   "pairs_per_step": len(units), "bytes_per_step_per_rank": step_bytes,
+        "config": workload_config(),
+        "method": {"bytes_per_step_per_rank_measured": step_bytes,
                    "l2": ("512 MB read flush between timed steps; 24 distinct input tensors, 2.3 GB read per "
                           "step (> L2)"),
                    "launch": ("eager launches" if args.no_graph else
