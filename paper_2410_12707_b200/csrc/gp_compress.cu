@@ -952,6 +952,10 @@ __global__ void __launch_bounds__(kCompressThreads, 1) compress_kernel(const Com
       fcreg[0] = (Key)sh_res[8];
       fcreg[1] = (Key)sh_res[9];
     }
+    // the rest of the 32-word window every CTA reads after B2 is written too
+    // (zeros past the keys): an unwritten sector of it would be read from DRAM
+    // on the critical path after an L2 flush, instead of from L2
+    if (!kDirectT && tid >= 2 && tid < 32 && tid - 2 >= sh_res[9]) fcreg[tid] = (Key)0;
     if (tid < 256) {
       sh_lvl[tid] = 0u;  // radix digit histograms of stage 3 (two levels, alternating)
       sh_low[tid] = 0u;
