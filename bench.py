@@ -765,7 +765,7 @@ class RefHostCodec:
             from oracle import compressor_oracle as R
         self.R = R
 
-    def compress(self, x, ratio):
+    def compress(self, x, ratio, frame=None):
         import torch
 
         host = x.detach().reshape(-1).float().cpu().numpy()
@@ -773,7 +773,11 @@ class RefHostCodec:
             raw = self.R.topk_compress(host, ratio).to_bytes()
         else:
             raw = self.R.compress_frame(host, ratio)
-        return torch.frombuffer(bytearray(raw), dtype=torch.uint8).to(x.device)
+        f = torch.frombuffer(bytearray(raw), dtype=torch.uint8)
+        if frame is not None:
+            frame.copy_(f)
+            return frame
+        return f.to(x.device)
 
     def decompress(self, frame, out, ratio):
         import numpy as np

@@ -42,6 +42,7 @@ extern "C" {
 #define GP_FLAG_UNSORTED      2u   /* indices not strictly increasing (fast path invalid) */
 #define GP_FLAG_HEADER        4u   /* frame header {d,k} disagrees with the receiver's (d, k / k_cap) */
 #define GP_FLAG_BAD_K         8u   /* device-resident k outside [1, min(k_cap, d)] (compress) */
+#define GP_FLAG_ENVELOPE     16u   /* a message's OpData envelope differs from what the receiver expects */
 
 /* Wire frame of the reference (compressor.py:39-44): little-endian
  * {d:u64, k:u64} header, k x i64 indices, k x f32 values. */
@@ -154,6 +155,22 @@ int gp_pack_frame(const void* idx, int idx_bytes, const void* vals, int val_dtyp
  * Replaces SparsePayload.from_bytes, compressor.py:46-53. */
 int gp_unpack_frame(const void* frame, int64_t k_cap, int64_t d_expect, int64_t* idx_out, void* vals_out,
                     int val_dtype, int64_t* hdr_out, uint32_t* d_err_flag, void* stream);
+
+/* ---- OpData envelope.  The reference wraps every cross-device payload in an
+ * OpData (opdag.py:67-86: producer, consumers, iteration, micro-batch,
+ * compress_cfg {algo, shape}) and routes it by those fields
+ * (executor.py:248-297).  Here a 128-byte envelope of GP_ENVELOPE_WORDS int64
+ * travels ahead of each stage-boundary message in the same buffer; the
+ * fields are the caller's (the Python transport uses: magic, iteration,
+ * micro-batch, source stage, destination stage, kind, compressed flag,
+ * payload bytes, ndim, shape[4]).  Both calls are stream-ordered kernels with
+ * the fields passed by value (no host copy); a mismatch in any field selected
+ * by `mask` raises GP_FLAG_ENVELOPE. */
+#define GP_ENVELOPE_WORDS 16
+#define GP_ENVELOPE_BYTES (GP_ENVELOPE_WORDS * 8)
+int gp_envelope_write(void* env_dev, const int64_t* fields, void* stream);
+int gp_envelope_check(const void* env_dev, const int64_t* expected, uint64_t mask, uint32_t* d_err_flag,
+                      void* stream);
 
 /* General scatter for arbitrary (unsorted, possibly repeated) indices with
  * numpy's last-write-wins semantics for `out[indices] = values`.  `scratch`

@@ -19,6 +19,9 @@ FLAG_OUT_OF_RANGE = 1
 FLAG_UNSORTED = 2
 FLAG_HEADER = 4   # frame header {d, k} disagrees with the receiver's expectation
 FLAG_BAD_K = 8    # device-resident k outside [1, min(k_cap, d)]
+FLAG_ENVELOPE = 16  # a message's OpData envelope differs from the receiver's expectation
+ENVELOPE_WORDS = 16
+ENVELOPE_BYTES = 128
 FRAME_HEADER_BYTES = 16
 
 _SIGS = {
@@ -44,6 +47,8 @@ _SIGS = {
     "gp_topk_decompress_frame_dk": (c_int, [c_void_p, c_int64, c_int64, c_void_p, c_int, c_int, c_void_p,
                                             c_void_p]),
     "gp_pack_frame": (c_int, [c_void_p, c_int, c_void_p, c_int, c_int64, c_int64, c_void_p, c_void_p]),
+    "gp_envelope_write": (c_int, [c_void_p, POINTER(c_int64), c_void_p]),
+    "gp_envelope_check": (c_int, [c_void_p, POINTER(c_int64), ctypes.c_uint64, c_void_p, c_void_p]),
     "gp_unpack_frame": (c_int, [c_void_p, c_int64, c_int64, c_void_p, c_void_p, c_int, c_void_p, c_void_p,
                                 c_void_p]),
     "gp_topk_decompress_unsorted": (c_int, [c_void_p, c_int, c_void_p, c_int, c_int64, c_int64, c_void_p, c_int,

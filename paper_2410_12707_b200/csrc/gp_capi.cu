@@ -249,6 +249,41 @@ int gp_topk_decompress_frame_dk(const void* frame, int64_t d, int64_t k_cap, voi
                            d_err_flag, stream, nullptr, f, 1);
 }
 
+// ---- OpData envelope (opdag.py:67-86) ahead of a stage-boundary message
+namespace {
+struct Envelope {
+  long long f[GP_ENVELOPE_WORDS];
+};
+
+__global__ void envelope_write_kernel(long long* env, Envelope e) {
+  if (threadIdx.x < GP_ENVELOPE_WORDS) env[threadIdx.x] = e.f[threadIdx.x];
+}
+
+__global__ void envelope_check_kernel(const long long* env, Envelope e, unsigned long long mask, uint32_t* err) {
+  const int i = threadIdx.x;
+  const bool bad = i < GP_ENVELOPE_WORDS && ((mask >> i) & 1ull) && env[i] != e.f[i];
+  if (__any_sync(0xFFFFFFFFu, bad) && i == 0) atomicOr(err, GP_FLAG_ENVELOPE);
+}
+}  // namespace
+
+int gp_envelope_write(void* env_dev, const int64_t* fields, void* stream) {
+  if (!env_dev || !fields || ((uintptr_t)env_dev % 8) != 0) return GP_ERR_INVALID_ARGUMENT;
+  Envelope e;
+  for (int i = 0; i < GP_ENVELOPE_WORDS; ++i) e.f[i] = fields[i];
+  envelope_write_kernel<<<1, 32, 0, as_stream(stream)>>>(static_cast<long long*>(env_dev), e);
+  return cudaGetLastError() == cudaSuccess ? GP_OK : GP_ERR_CUDA;
+}
+
+int gp_envelope_check(const void* env_dev, const int64_t* expected, uint64_t mask, uint32_t* d_err_flag,
+                      void* stream) {
+  if (!env_dev || !expected || !d_err_flag || ((uintptr_t)env_dev % 8) != 0) return GP_ERR_INVALID_ARGUMENT;
+  Envelope e;
+  for (int i = 0; i < GP_ENVELOPE_WORDS; ++i) e.f[i] = expected[i];
+  envelope_check_kernel<<<1, 32, 0, as_stream(stream)>>>(static_cast<const long long*>(env_dev), e,
+                                                          (unsigned long long)mask, d_err_flag);
+  return cudaGetLastError() == cudaSuccess ? GP_OK : GP_ERR_CUDA;
+}
+
 // ---- standalone frame pack / unpack (SparsePayload.to_bytes / from_bytes, compressor.py:39-53)
 namespace {
 __device__ __forceinline__ float val_as_f32(const void* v, int dt, int64_t j) {

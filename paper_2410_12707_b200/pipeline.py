@@ -30,7 +30,8 @@ import torch.nn as nn
 import torch.nn.functional as F
 
 from .compressor import CompressionPlan, adatopk_plan, adatopk_plan_device, select_k, uniform_plan
-from .transport import FrameCodec, frame_bytes
+from .transport import (ENVELOPE_BYTES, KIND_ACTIVATION, KIND_GRADIENT, FrameCodec, check_envelope, envelope_fields,
+                        frame_bytes, write_envelope)
 
 _P2P_BATCHED = os.environ.get("GP_P2P_BATCHED", "1") == "1"  # batched single-op P2P (0: plain isend/irecv)
 
@@ -468,6 +469,12 @@ class DistPipeline:
         self.opt = torch.optim.AdamW(self.stage.parameters(), lr=lr)
         self.codec = codec if codec is not None else FrameCodec(self.device)
         self.shape = (micro_batch, seq_len, cfg.n_embd)
+        self.step_no = 0    # the iteration in every message envelope (OpData.local_iter)
+        # device flag of the envelope checks: the codec's own (read by its check()), or, for a codec
+        # without one (host baselines), the pipeline's
+        self._err = getattr(self.codec, "err", None)
+        if self._err is None and self.device.type == "cuda":
+            self._err = torch.zeros(1, dtype=torch.int32, device=self.device)
         self.messages = []  # (direction, src_stage, dst_stage, micro_batch) in send order (tests)
 
     def _amp(self):
@@ -490,28 +497,49 @@ class DistPipeline:
             return dist.batch_isend_irecv([dist.P2POp(op, buf, peer)])[0]
         return op(buf, peer)
 
-    def _send(self, x: torch.Tensor, dst: int):
-        """Send stage self.s's tensor to stage dst (link keys are stage indices)."""
-        link = (self.s, dst)
+    def _payload_bytes(self, link) -> tuple:
+        """(compressed, payload bytes) of a message on `link` (the receiver sizes its buffer from these)."""
+        d = math.prod(self.shape)
         if self.dev_plan is not None and link in self.dev_plan.index:
-            buf = self.codec.compress_dk(x.detach().contiguous(), self.dev_plan.k_slot(link), self.dev_plan.k_cap)
+            return True, 16 + 12 * self.dev_plan.k_cap
+        r = self._ratio(*link)
+        return (False, 4 * d) if r <= 1.0 else (True, frame_bytes(d, r))
+
+    def _send(self, x: torch.Tensor, dst: int, m: int, kind: int):
+        """Send stage self.s's tensor to stage dst (link keys are stage indices) as one
+        buffer: the OpData envelope (transport.envelope_fields), then the payload --
+        a reference wire frame written in place by the compress kernel, or the dense
+        tensor (ratio <= 1, executor.py:210-212)."""
+        link = (self.s, dst)
+        x = x.detach().contiguous()
+        compressed, nbytes = self._payload_bytes(link)
+        buf = torch.empty(ENVELOPE_BYTES + nbytes, dtype=torch.uint8, device=self.device)
+        write_envelope(buf, envelope_fields(self.step_no, m, self.s, dst, kind, compressed, nbytes, x.shape))
+        body = buf[ENVELOPE_BYTES:]
+        if self.dev_plan is not None and link in self.dev_plan.index:
+            self.codec.compress_dk(x, self.dev_plan.k_slot(link), self.dev_plan.k_cap, frame=body)
+        elif compressed:
+            self.codec.compress(x, self._ratio(*link), frame=body)
         else:
-            r = self._ratio(*link)
-            buf = x.detach().contiguous() if r <= 1.0 else self.codec.compress(x.detach().contiguous(), r)
+            body.view(x.dtype).copy_(x.reshape(-1))
         return self._p2p(dist.isend, buf, dst), buf
 
-    def _recv(self, src: int) -> torch.Tensor:
+    def _recv(self, src: int, m: int, kind: int) -> torch.Tensor:
         link = (src, self.s)
         out = torch.empty(self.shape, device=self.device)
-        if self.dev_plan is not None and link in self.dev_plan.index:
-            k_cap = self.dev_plan.k_cap
-            buf = torch.empty(16 + 12 * k_cap, dtype=torch.uint8, device=self.device)
-            self._p2p(dist.irecv, buf, src).wait()
-            return self.codec.decompress_dk(buf, out, k_cap)
-        r = self._ratio(*link)
-        buf = out if r <= 1.0 else torch.empty(frame_bytes(out.numel(), r), dtype=torch.uint8, device=self.device)
+        compressed, nbytes = self._payload_bytes(link)
+        buf = torch.empty(ENVELOPE_BYTES + nbytes, dtype=torch.uint8, device=self.device)
         self._p2p(dist.irecv, buf, src).wait()
-        return out if r <= 1.0 else self.codec.decompress(buf, out, r)
+        # the envelope the sender must have written for this (iteration, micro-batch, link, kind)
+        check_envelope(buf, envelope_fields(self.step_no, m, src, self.s, kind, compressed, nbytes, self.shape),
+                       self._err)
+        body = buf[ENVELOPE_BYTES:]
+        if self.dev_plan is not None and link in self.dev_plan.index:
+            return self.codec.decompress_dk(body, out, self.dev_plan.k_cap)
+        if not compressed:
+            out.reshape(-1).copy_(body.view(out.dtype))
+            return out
+        return self.codec.decompress(body, out, self._ratio(*link))
 
     def forward_only(self, tokens: torch.Tensor, targets: torch.Tensor, n_micro: int):
         """The FP half of a step (fill phase, no backward): what Eq. 3 / Eq. 7 model."""
@@ -520,13 +548,14 @@ class DistPipeline:
         pending = []
         with torch.no_grad():
             for m in range(n_micro):
-                inp = mbs[m] if s == 0 else self._recv(s - 1)
+                inp = mbs[m] if s == 0 else self._recv(s - 1, m, KIND_ACTIVATION)
                 with self._amp():
                     y = self.stage(inp, tgs[m] if s == S - 1 else None)
                 if s < S - 1:
-                    pending.append(self._send(y, s + 1))
+                    pending.append(self._send(y, s + 1, m, KIND_ACTIVATION))
         for w, _buf in pending:
             w.wait()
+        self.step_no += 1
 
     def stage_fp_time(self, tokens: torch.Tensor, targets: torch.Tensor, reps: int = 5) -> float:
         """C_d: this stage's forward time for one micro-batch (s, CUDA events, median)."""
@@ -554,12 +583,12 @@ class DistPipeline:
         mbs, tgs = tokens.chunk(n_micro), targets.chunk(n_micro)
         pending, saved, losses = [], [], []
         for m in range(n_micro):  # fill
-            inp = mbs[m] if s == 0 else self._recv(s - 1).requires_grad_(True)
+            inp = mbs[m] if s == 0 else self._recv(s - 1, m, KIND_ACTIVATION).requires_grad_(True)
             with self._amp():
                 y = self.stage(inp, tgs[m] if s == S - 1 else None)
             saved.append((inp, y))
             if s < S - 1:
-                pending.append(self._send(y, s + 1))
+                pending.append(self._send(y, s + 1, m, KIND_ACTIVATION))
                 self.messages.append(("fp", s, s + 1, m))
             else:
                 losses.append(y.detach())
@@ -568,9 +597,9 @@ class DistPipeline:
             if s == S - 1:
                 (y / n_micro).backward()
             else:
-                y.backward(self._recv(s + 1))
+                y.backward(self._recv(s + 1, m, KIND_GRADIENT))
             if s > 0:
-                pending.append(self._send(inp.grad, s - 1))
+                pending.append(self._send(inp.grad, s - 1, m, KIND_GRADIENT))
                 self.messages.append(("bp", s, s - 1, m))
         for w, _buf in pending:
             w.wait()
@@ -578,8 +607,12 @@ class DistPipeline:
         self.opt.zero_grad(set_to_none=True)
         loss = torch.stack(losses).mean() if losses else torch.zeros((), device=self.device)
         dist.broadcast(loss, self.chain[S - 1])
+        self.step_no += 1
         if check and hasattr(self.codec, "check"):
             self.codec.check()  # one flag read per step: a corrupt received frame raises here
+        elif check and self._err is not None and int(self._err.item()):
+            self._err.zero_()
+            raise ValueError("a received message's OpData envelope differs from the receiver's expectation")
         return float(loss)
 
 

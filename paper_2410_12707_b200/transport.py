@@ -16,6 +16,8 @@ pure function — so no size handshake precedes the payload.
 """
 from __future__ import annotations
 
+import ctypes
+import math
 from dataclasses import dataclass
 from typing import Optional
 
@@ -47,6 +49,59 @@ def maybe_decompress(payload, shape):
 
 def frame_bytes(d: int, ratio: float) -> int:
     return 16 + 12 * select_k(d, ratio)
+
+
+# ---------------------------------------------------------------------------
+# OpData envelope (opdag.py:67-86): the reference routes every cross-device
+# payload in an OpData carrying the producer, consumers, iteration,
+# micro-batch and compress_cfg {algo, shape} (executor.py:259-268, :283-292).
+# Here a 128-byte envelope of 16 int64 travels ahead of each stage-boundary
+# message in the same buffer, written and checked on the device.
+
+ENVELOPE_BYTES = _lib.ENVELOPE_BYTES
+ENVELOPE_MAGIC = 0x41504F4441544131  # "1ATADOPA": an OpData envelope, layout version 1
+KIND_ACTIVATION, KIND_GRADIENT = 0, 1
+ENVELOPE_ALL = (1 << _lib.ENVELOPE_WORDS) - 1
+
+
+def envelope_fields(step: int, micro_batch: int, src: int, dst: int, kind: int, compressed: bool,
+                    payload_bytes: int, shape) -> list:
+    """[magic, iteration (local_iter), micro_batch, src stage, dst stage, kind (0 activation, 1
+    gradient), compressed (compress_cfg algo 'topk'), payload bytes, ndim, shape[4], 0, 0, 0]."""
+    shape = [int(v) for v in shape]
+    if len(shape) > 4:
+        shape = shape[:3] + [int(math.prod(shape[3:]))]
+    return ([ENVELOPE_MAGIC, int(step), int(micro_batch), int(src), int(dst), int(kind), int(bool(compressed)),
+             int(payload_bytes), len(shape)] + shape + [0] * (4 - len(shape)) + [0, 0, 0])
+
+
+def write_envelope(buf: torch.Tensor, fields: list) -> None:
+    """Write the envelope into the first 128 bytes of a uint8 message buffer (stream-ordered on a GPU)."""
+    if buf.is_cuda:
+        with torch.cuda.device(buf.device):
+            st = _lib.lib().gp_envelope_write(buf.data_ptr(), (ctypes.c_int64 * _lib.ENVELOPE_WORDS)(*fields),
+                                              _stream_handle(buf.device))
+        raise_for_status(st, "gp_envelope_write")
+    else:
+        buf[:ENVELOPE_BYTES].view(torch.int64).copy_(torch.tensor(fields, dtype=torch.int64))
+
+
+def check_envelope(buf: torch.Tensor, expected: list, err: Optional[torch.Tensor] = None,
+                   mask: int = ENVELOPE_ALL) -> None:
+    """Compare a received envelope with the receiver's expectation: on a GPU a
+    stream-ordered check raising GP_FLAG_ENVELOPE in `err` (read at the step's
+    flag check); on CPU ranks at once (ValueError)."""
+    if buf.is_cuda:
+        with torch.cuda.device(buf.device):
+            st = _lib.lib().gp_envelope_check(buf.data_ptr(), (ctypes.c_int64 * _lib.ENVELOPE_WORDS)(*expected),
+                                              mask, err.data_ptr(), _stream_handle(buf.device))
+        raise_for_status(st, "gp_envelope_check")
+        return
+    got = buf[:ENVELOPE_BYTES].view(torch.int64).tolist()
+    bad = [i for i in range(_lib.ENVELOPE_WORDS) if (mask >> i) & 1 and got[i] != expected[i]]
+    if bad:
+        raise ValueError(f"message envelope fields {bad} are {[got[i] for i in bad]}, expected "
+                         f"{[expected[i] for i in bad]}")
 
 
 @dataclass
@@ -140,6 +195,8 @@ class FrameCodec:
             raise ValueError("received frame header {d, k} disagrees with the receiver's (d, k)")
         if flag & _lib.FLAG_BAD_K:
             raise ValueError("device-resident k outside [1, min(k_cap, d)]")
+        if flag & _lib.FLAG_ENVELOPE:
+            raise ValueError("a received message's OpData envelope differs from the receiver's expectation")
 
 
 class StageLink:
@@ -199,4 +256,5 @@ def payload_from_frame(frame: torch.Tensor, values_dtype=torch.float32) -> Spars
     return SparsePayload(values=vals, indices=idx, original_len=d, frame=frame)
 
 
-__all__ = ["maybe_compress", "maybe_decompress", "frame_bytes", "FrameCodec", "StageLink", "payload_from_frame"]
+__all__ = ["maybe_compress", "maybe_decompress", "frame_bytes", "FrameCodec", "StageLink", "payload_from_frame",
+           "ENVELOPE_BYTES", "envelope_fields", "write_envelope", "check_envelope", "KIND_ACTIVATION", "KIND_GRADIENT"]

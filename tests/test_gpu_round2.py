@@ -276,3 +276,20 @@ def test_one_workspace_serves_every_fitting_call(cuda):
                 assert L.gp_topk_compress_frame(x.data_ptr(), dt, n, k, frame.data_ptr(), ws.data_ptr(), wsb, sp) == 0
                 host = x.float().cpu().numpy() if dt == 1 else x.cpu().numpy()
                 assert frame.cpu().numpy().tobytes() == O.compress_frame(host, r, method="threshold"), (rep, n, dt, r)
+
+
+def test_opdata_envelope_device(cuda):
+    """Envelope written and checked by stream-ordered kernels (fields passed by
+    value); a mismatch raises GP_FLAG_ENVELOPE, read at the step's flag check."""
+    from paper_2410_12707_b200 import transport as T
+
+    codec = FrameCodec(cuda)
+    f = T.envelope_fields(7, 2, 0, 1, T.KIND_ACTIVATION, True, 4096, (8, 1024, 768))
+    buf = torch.empty(T.ENVELOPE_BYTES + 64, dtype=torch.uint8, device=cuda)
+    T.write_envelope(buf, f)
+    assert buf[:T.ENVELOPE_BYTES].view(torch.int64).tolist() == f
+    T.check_envelope(buf, f, codec.err)
+    codec.check()
+    T.check_envelope(buf, T.envelope_fields(7, 3, 0, 1, T.KIND_ACTIVATION, True, 4096, (8, 1024, 768)), codec.err)
+    with pytest.raises(ValueError, match="envelope"):
+        codec.check()

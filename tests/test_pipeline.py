@@ -22,9 +22,13 @@ REL_TOL = 1e-3
 class OracleCodec:
     """Boundary codec through the CPU reference compressor (test baseline only)."""
 
-    def compress(self, x, ratio):
+    def compress(self, x, ratio, frame=None):
         raw = O.compress_frame(x.detach().reshape(-1).float().cpu().numpy(), ratio)
-        return torch.frombuffer(bytearray(raw), dtype=torch.uint8).to(x.device)
+        f = torch.frombuffer(bytearray(raw), dtype=torch.uint8).to(x.device)
+        if frame is not None:
+            frame.copy_(f)
+            return frame
+        return f
 
     def decompress(self, frame, out, ratio):
         vals, idx, d = O.from_bytes(frame.cpu().numpy().tobytes())

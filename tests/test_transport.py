@@ -23,8 +23,12 @@ from paper_2410_12707_b200.compressor import CompressionPlan
 class OracleCodec:
     """CPU codec producing the reference frame with the oracle (test only)."""
 
-    def compress(self, x, ratio):
-        return torch.frombuffer(bytearray(O.compress_frame(x.reshape(-1).numpy(), ratio)), dtype=torch.uint8)
+    def compress(self, x, ratio, frame=None):
+        f = torch.frombuffer(bytearray(O.compress_frame(x.reshape(-1).numpy(), ratio)), dtype=torch.uint8)
+        if frame is not None:
+            frame.copy_(f)
+            return frame
+        return f
 
     def decompress(self, frame, out, ratio):
         vals, idx, d = O.from_bytes(frame.numpy().tobytes())
@@ -265,3 +269,16 @@ def test_peer_ring_world2(cuda, pull, shared):
     for p in ps:
         p.join(timeout=60)
     assert res == {0: True, 1: True}, res
+
+
+def test_opdata_envelope_cpu():
+    """The OpData envelope (opdag.py:67-86) ahead of every pipeline message:
+    iteration, micro-batch, link, kind, compress_cfg and shape; a receiver
+    expecting anything else raises."""
+    f = T.envelope_fields(3, 5, 1, 2, T.KIND_GRADIENT, True, 1234, (2, 64, 128))
+    assert f[:9] == [T.ENVELOPE_MAGIC, 3, 5, 1, 2, 1, 1, 1234, 3] and f[9:12] == [2, 64, 128]
+    buf = torch.zeros(T.ENVELOPE_BYTES + 16, dtype=torch.uint8)
+    T.write_envelope(buf, f)
+    T.check_envelope(buf, f)
+    with pytest.raises(ValueError, match="envelope"):
+        T.check_envelope(buf, T.envelope_fields(3, 6, 1, 2, T.KIND_GRADIENT, True, 1234, (2, 64, 128)))
