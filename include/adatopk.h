@@ -88,6 +88,12 @@ int gp_topk_compress(const void* x, int dtype, int64_t d, int64_t k,
 int gp_topk_compress_frame(const void* x, int dtype, int64_t d, int64_t k,
                            void* frame_out, void* ws, size_t ws_bytes, void* stream);
 
+/* decompress `mode` bits */
+#define GP_DECOMPRESS_RESIDUAL 1   /* add into `out` instead of zero-filling (extension) */
+#define GP_DECOMPRESS_TRUSTED  2   /* indices written by gp_topk_compress* and unmodified: strictly
+                                      increasing by construction, so the O(k) sortedness scan is skipped
+                                      (the O(1) range check and the frame header check remain) */
+
 /* Dense length-d output: values at their indices, zero (mode 0) or added to
  * the existing contents (mode 1, residual extension) elsewhere.  Fast path,
  * requires strictly increasing indices; violations and out-of-range indices are

@@ -362,11 +362,14 @@ def _topk_decompress_on(payload, device: torch.device, out, accumulate: bool, ch
     err = _Flags.get(device, sp)
     L = _lib.lib()
     ib = indices.element_size()
+    # a kernel-made, unmodified payload is valid by construction: no sortedness
+    # scan on the device (GP_DECOMPRESS_TRUSTED) and no flag read on the host
+    trusted = getattr(payload, "_kernel_made", False) and payload._unmodified()
     st = L.gp_topk_decompress(indices.data_ptr(), ib, values.data_ptr(), code, k, d, out.data_ptr(), out_code,
-                              1 if accumulate else 0, err.data_ptr(), sp)
+                              (1 if accumulate else 0) | (2 if trusted else 0), err.data_ptr(), sp)
     raise_for_status(st, "gp_topk_decompress", indices)
-    if check and getattr(payload, "_kernel_made", False) and payload._unmodified():
-        check = False  # a kernel-made, unmodified payload: the flag cannot be raised
+    if trusted:
+        check = False
     if check:
         flag = _Flags.read(err)
         if flag & _lib.FLAG_UNSORTED:

@@ -216,7 +216,7 @@ static int decompress_common(const void* idx, int idx_bytes, const void* vals, i
   if (k < 0 || d < 0) return GP_ERR_INVALID_ARGUMENT;
   if (idx_bytes != 4 && idx_bytes != 8) return GP_ERR_INVALID_ARGUMENT;
   if (val_dtype < 0 || val_dtype > 2 || out_dtype < 0 || out_dtype > 2) return GP_ERR_INVALID_ARGUMENT;
-  if (mode != 0 && mode != 1) return GP_ERR_INVALID_ARGUMENT;
+  if (mode < 0 || mode > 3) return GP_ERR_INVALID_ARGUMENT;  // GP_DECOMPRESS_RESIDUAL | GP_DECOMPRESS_TRUSTED
   if (!d_err_flag || (k > 0 && (!idx || (!vals && !dev_k))) || (d > 0 && !out)) return GP_ERR_INVALID_ARGUMENT;
   if (d == 0 && k > 0) return GP_ERR_INDEX_OUT_OF_RANGE;  // every index is >= d
   gp::DeviceInfo dev;

@@ -158,8 +158,11 @@ __device__ __forceinline__ bool pair_check_rest(const IT* __restrict__ idx, int6
 template <class IT, class VT, class OT>
 __global__ void __launch_bounds__(kDecThreads, kDecBlocksPerSm) decompress_kernel(
     const IT* __restrict__ idx, const VT* __restrict__ vals, int64_t k, int64_t d, int64_t chunk,
-    OT* __restrict__ out, int mode, uint32_t* err, unsigned long long* dbg, const unsigned long long* hdr, int dev_k) {
+    OT* __restrict__ out, int mode_bits, uint32_t* err, unsigned long long* dbg, const unsigned long long* hdr,
+    int dev_k) {
   constexpr int kTileElems = kTileBytes / (int)sizeof(OT);
+  const int mode = mode_bits & 1;                // 1: residual add
+  const bool trusted = (mode_bits & 2) != 0;     // indices from gp_topk_compress: no sortedness scan
   if (hdr != nullptr) {  // the frame's {d, k} header against what the receiver expects
     const unsigned long long hd = __ldg(hdr), hk = __ldg(hdr + 1);
     const bool ok = hd == (unsigned long long)d &&
@@ -193,7 +196,7 @@ __global__ void __launch_bounds__(kDecThreads, kDecBlocksPerSm) decompress_kerne
   // This CTA's 1/grid share of the k-1 adjacent-pair checks (covers every
   // pair whatever the input); the first pair per thread is loaded now and
   // compared at the end, so its latency overlaps the rest.
-  const int64_t P = k > 1 ? k - 1 : 0;
+  const int64_t P = (k > 1 && !trusted) ? k - 1 : 0;  // adjacent pairs this launch checks
   const int64_t pb = (P * (int64_t)blockIdx.x) / gridDim.x;
   const int64_t pe = (P * ((int64_t)blockIdx.x + 1)) / gridDim.x;
   int64_t pa = 0, pz = 1;
@@ -339,7 +342,7 @@ __global__ void __launch_bounds__(kDecThreads, kDecBlocksPerSm) decompress_kerne
 template <class IT, class VT, class OT>
 __global__ void __launch_bounds__(kDecThreads, kDecBlocksPerSm) decompress_sparse_kernel(
     const IT* __restrict__ idx, const VT* __restrict__ vals, int64_t k, int64_t d, int64_t chunk,
-    OT* __restrict__ out, uint32_t* err, const unsigned long long* hdr, int dev_k) {
+    OT* __restrict__ out, uint32_t* err, const unsigned long long* hdr, int dev_k, bool trusted) {
   if (hdr != nullptr) {  // the frame's {d, k} header against what the receiver expects
     const unsigned long long hd = __ldg(hdr), hk = __ldg(hdr + 1);
     const bool ok = hd == (unsigned long long)d &&
@@ -356,7 +359,7 @@ __global__ void __launch_bounds__(kDecThreads, kDecBlocksPerSm) decompress_spars
   const int64_t o0 = min((int64_t)blockIdx.x * chunk, d);
   const int64_t o1 = min(o0 + chunk, d);
   bool bad = false;
-  const int64_t P = k > 1 ? k - 1 : 0;
+  const int64_t P = (k > 1 && !trusted) ? k - 1 : 0;  // adjacent pairs this launch checks
   const int64_t pb = (P * (int64_t)blockIdx.x) / gridDim.x;
   const int64_t pe = (P * ((int64_t)blockIdx.x + 1)) / gridDim.x;
   int64_t pa = 0, pz = 1;
@@ -462,9 +465,9 @@ static int run_fast(const DecompressArgs& a, const DeviceInfo& dev, cudaStream_t
       return 5;
     carveout_set[dev.ordinal].store(true, std::memory_order_release);
   }
-  if (a.mode == 0 && a.k * kSparseDensityInv <= a.d && a.d * (int64_t)sizeof(OT) <= kSparseMaxBytes) {
+  if ((a.mode & 1) == 0 && a.k * kSparseDensityInv <= a.d && a.d * (int64_t)sizeof(OT) <= kSparseMaxBytes) {
     decompress_sparse_kernel<IT, VT, OT><<<(unsigned)grid, kDecThreads, 0, s>>>(
-        (const IT*)a.idx, (const VT*)a.vals, a.k, a.d, chunk, (OT*)a.out, a.err, a.hdr, a.dev_k);
+        (const IT*)a.idx, (const VT*)a.vals, a.k, a.d, chunk, (OT*)a.out, a.err, a.hdr, a.dev_k, (a.mode & 2) != 0);
   } else {
     decompress_kernel<IT, VT, OT><<<(unsigned)grid, kDecThreads, kTileBufs * kTileBytes, s>>>(
         (const IT*)a.idx, (const VT*)a.vals, a.k, a.d, chunk, (OT*)a.out, a.mode, a.err, a.dbg, a.hdr, a.dev_k);

@@ -293,3 +293,33 @@ def test_opdata_envelope_device(cuda):
     T.check_envelope(buf, T.envelope_fields(7, 3, 0, 1, T.KIND_ACTIVATION, True, 4096, (8, 1024, 768)), codec.err)
     with pytest.raises(ValueError, match="envelope"):
         codec.check()
+
+
+@pytest.mark.parametrize("ratio", [3.0, 10.0, 100.0])
+def test_trusted_decompress_equals_checked(cuda, ratio):
+    """GP_DECOMPRESS_TRUSTED (a frame gp_topk_compress just wrote: strictly
+    increasing by construction) skips only the O(k) sortedness scan: the output
+    is bit-identical to the checked decompress, in zero and residual mode, and a
+    frame with an out-of-range index is still flagged (the range check stays)."""
+    L = _lib.lib()
+    codec = FrameCodec(cuda)
+    g = torch.Generator(device=cuda).manual_seed(50)
+    x = torch.randn(3_000_017, device=cuda, generator=g)
+    d, k = x.numel(), O.select_k(x.numel(), ratio)
+    frame = codec.compress(x, ratio)
+    sp = torch.cuda.current_stream().cuda_stream
+    err = torch.zeros(1, dtype=torch.int32, device=cuda)
+    base = torch.randn(d, device=cuda, generator=g)
+    for mode in (0, 1):
+        a, b = base.clone(), base.clone()
+        assert L.gp_topk_decompress_frame(frame.data_ptr(), k, d, a.data_ptr(), 0, mode, err.data_ptr(), sp) == 0
+        assert L.gp_topk_decompress_frame(frame.data_ptr(), k, d, b.data_ptr(), 0, mode | 2, err.data_ptr(), sp) == 0
+        assert torch.equal(a.view(torch.int32), b.view(torch.int32)) and int(err.item()) == 0
+    bad = frame.clone()
+    bad[16:16 + 8 * k].view(torch.int64)[-1] = d + 7
+    assert L.gp_topk_decompress_frame(bad.data_ptr(), k, d, base.data_ptr(), 0, 2, err.data_ptr(), sp) == 0
+    assert int(err.item()) & _lib.FLAG_OUT_OF_RANGE
+    p = P.topk_compress(x, ratio)  # the drop-in: kernel-made payloads decompress trusted, no host sync
+    ref = torch.zeros_like(x)
+    ref[p.indices] = x[p.indices]
+    assert torch.equal(P.topk_decompress(p).view(torch.int32), ref.view(torch.int32))
