@@ -65,6 +65,9 @@ constexpr uint32_t kFcCapBig = 65536;  // final candidates the fast path accepts
 #ifndef GP_DEFER_REST
 #define GP_DEFER_REST 1
 #endif
+#ifndef GP_SKIP_EMPTY
+#define GP_SKIP_EMPTY 0
+#endif
 #ifndef GP_WM_REFINE
 #define GP_WM_REFINE 1
 #endif
@@ -666,6 +669,11 @@ __global__ void __launch_bounds__(kCompressThreads, 1) compress_kernel(const Com
           m[j] = mm;
         }
       }
+#if GP_SKIP_EMPTY
+      // no candidate anywhere in the step (about a quarter of the steps at
+      // r = 1000 with the refined watermark): done after one vote
+      if (!__any_sync(kFull, (m[0] | m[1] | m[2] | m[3]) != 0u)) return;
+#endif
       // per-sub-row counts packed into one scan: 8-bit fields when a sub-row
       // holds at most 32*EPS <= 128 candidates (f32, f64), else 16-bit fields
       constexpr int kField = EPS * 32 < 256 ? 8 : 16;
@@ -681,6 +689,9 @@ __global__ void __launch_bounds__(kCompressThreads, 1) compress_kernel(const Com
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
           const uint32_t bj = __ballot_sync(kFull, m[j] != 0u);
+#if GP_SKIP_EMPTY
+          if (bj == 0u) continue;  // warp-uniform: no candidate in this sub-row
+#endif
           if (m[j]) {
             const uint32_t e = __ffs(m[j]) - 1;
             const uint32_t piece = (j & 1) * 32u + lane;
