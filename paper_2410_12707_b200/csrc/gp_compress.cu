@@ -1012,6 +1012,7 @@ __global__ void __launch_bounds__(kCompressThreads, 1) compress_kernel(const Com
       }
     }
     extra = __syncthreads_or(extra);
+    STAMP(9);
     // Keys beyond the first kSpec-2 of a CTA (many FC keys, e.g. r = 10 on a
     // large tensor) are fetched once, in one round trip, into sh_fckey
     // (flattened; sh_fcoff[c2] = offset of CTA c2's extras, sh_fcoff[G] = total).
@@ -1178,6 +1179,7 @@ __global__ void __launch_bounds__(kCompressThreads, 1) compress_kernel(const Com
       }
     }
     __syncthreads();
+    STAMP(10);
     const uint32_t eq_before = sh_res[25];  // key == T final candidates in earlier CTAs
     const uint32_t kept_eq0 = min(eq_before, need_eq);
     // kept own final candidates before own FC position p

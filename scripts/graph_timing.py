@@ -130,6 +130,12 @@ def main():
                         parts.append(f"{STAGES[i - 1]}={np.mean(delta) / 1e3:.2f}/{np.max(delta) / 1e3:.2f}")
                 print(f"    {label} G={G} skew={(ns[:, 0].max() - t00) / 1e3:.2f} "
                       f"end={(ns[:, 8].max() - t00) / 1e3:.2f}us " + " ".join(parts), flush=True)
+                sub = a[:G, :11].astype(np.int64)
+                if (sub[:, 9] > 0).all() and (sub[:, 10] > 0).all():  # fast-path stage-3 split (stamps 9, 10)
+                    print(f"      stage3: gather={np.mean(sub[:, 9] - sub[:, 6]) / 1e3:.2f} "
+                          f"select={np.mean(sub[:, 7] - sub[:, 9]) / 1e3:.2f} "
+                          f"prefix={np.mean(sub[:, 10] - sub[:, 7]) / 1e3:.2f} "
+                          f"walk={np.mean(sub[:, 8] - sub[:, 10]) / 1e3:.2f}", flush=True)
 
 
 if __name__ == "__main__":
