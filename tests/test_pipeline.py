@@ -112,6 +112,48 @@ def test_gpt2_loss_parity_10_steps_vs_oracle_codec(cuda, model):
     assert gpu[-1] < gpu[0]
 
 
+def _periodic_batch(cfg, batch, seq_len, device, seed):
+    """A learnable synthetic task: each sequence counts up from a random start
+    with a per-sequence stride (next token = token + stride mod V)."""
+    g = torch.Generator(device=device).manual_seed(seed)
+    start = torch.randint(0, cfg.vocab, (batch, 1), device=device, generator=g)
+    stride = torch.randint(1, 4, (batch, 1), device=device, generator=g)
+    pos = torch.arange(seq_len + 1, device=device).unsqueeze(0)
+    tok = (start + stride * pos) % cfg.vocab
+    return tok[:, :-1].contiguous(), tok[:, 1:].contiguous()
+
+
+@pytest.mark.gpu
+def test_compressed_pipeline_tracks_dense_training(cuda):
+    """The reference's convergence criterion (tests/test_cli.py:155-164: AdaTopK
+    at ratio 10 keeps >= half of the uncompressed loss reduction after 20
+    iterations) on the GPU pipeline: 2 stages, the activation link compressed
+    at r = 10 by the sm_100a codec as in the reference CLI's plans (which key FP
+    links only, SURVEY.md §7 hard part 10), on a learnable task; compressing
+    the gradient link too still learns."""
+    cfg = PL.GPT2Config(4, 128, 4, vocab=256, n_ctx=64)
+
+    def run(plan):
+        torch.manual_seed(0)
+        pipe = PL.VirtualPipeline(cfg, 2, plan, cuda, lr=3e-3, seed=11)
+        out = []
+        for i in range(20):
+            tok, tgt = _periodic_batch(cfg, 16, 64, cuda, seed=i)
+            out.append(pipe.step(tok, tgt, n_micro=4))
+        return out, pipe.stats
+
+    from paper_2410_12707_b200.compressor import CompressionPlan
+
+    dense, _ = run(None)
+    comp, st = run(CompressionPlan(base_ratio=10.0, per_link={(0, 1): 10.0}))
+    both, st2 = run(PL.link_plan(2, "uniform", 10.0))
+    assert st.compress_calls == 20 * 4 and st2.compress_calls == 20 * 4 * 2 and st.wire_bytes < st.dense_bytes
+    start = dense[0]
+    assert start - dense[-1] > 0.5  # the task is learnable in 20 steps
+    assert (start - comp[-1]) >= 0.5 * (start - dense[-1]), (dense, comp)
+    assert start - both[-1] > 0.25 * (start - dense[-1]), (dense, both)
+
+
 @pytest.mark.gpu
 def test_compressed_pipeline_trains(cuda):
     losses, st = _losses(None, cuda, steps=12, plan_ratio=4.0)
