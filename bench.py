@@ -747,7 +747,9 @@ def run_ours(args, rank, world, local_rank):
             # configs[3]: GPT-2 XL, one stage per GPU (8 at N=8), stage -> GPU chain and block ranges from the
             # reference's unchanged OP-Fence over a simulated two-cluster network, Eq. 6 ratios from its
             # cross_link_times
-            sub("pipeline_xl_adatopk", "xl", "adatopk", 100.0, steps=3, warmup=2)
+            sub("pipeline_xl_adatopk", "xl", "adatopk", 100.0, steps=3, warmup=2,
+                trace_path=(os.path.join(os.environ["GP_BENCH_TRACE_DIR"], f"pipeline_xl_{world}gpu_trace.json")
+                            if os.environ.get("GP_BENCH_TRACE_DIR") else None))
             # the same pipeline with the reference's CPU compressor at the boundaries (host
             # round trip per message) next to the sm_100a codec on the identical configuration
             run, ckind, cname = _cpu_impl()

@@ -425,6 +425,46 @@ class DevicePlan:
         return self.k[i:i + 1]
 
 
+class _Timeline:
+    """CUDA-event spans of one pipeline step on this rank, exported in the
+    reference's Chrome trace format (simulator.py:75-95: complete "X" events,
+    microseconds) so a measured step can be laid next to the simulated one."""
+
+    def __init__(self):
+        self.t0 = torch.cuda.Event(enable_timing=True)
+        self.t0.record()
+        self.spans = []
+
+    def span(self, name: str, cat: str):
+        tl = self
+
+        class _Span:
+            def __enter__(self):
+                self.a = torch.cuda.Event(enable_timing=True)
+                self.a.record()
+
+            def __exit__(self, *exc):
+                b = torch.cuda.Event(enable_timing=True)
+                b.record()
+                tl.spans.append((name, cat, self.a, b))
+                return False
+
+        return _Span()
+
+    def events(self, pid, tid) -> list:
+        torch.cuda.synchronize()
+        return [{"name": n, "cat": c, "ph": "X", "ts": round(self.t0.elapsed_time(a) * 1e3, 3),
+                 "dur": round(a.elapsed_time(b) * 1e3, 3), "pid": pid, "tid": tid} for n, c, a, b in self.spans]
+
+
+class _NoSpan:
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        return False
+
+
 class _HostWork:
     """A gloo P2P request on a host staging buffer; `wait()` copies a received buffer to the device."""
 
@@ -574,37 +614,55 @@ class DistPipeline:
         ts = sorted(ts[1:])
         return ts[len(ts) // 2]
 
-    def step(self, tokens: torch.Tensor, targets: torch.Tensor, n_micro: int, check: bool = True):
+    def step(self, tokens: torch.Tensor, targets: torch.Tensor, n_micro: int, check: bool = True,
+             trace: bool = False):
         """One GPipe fill-drain iteration (executor.py:376-411): every micro-batch
         forward (activations to the next stage, _send_activation :248-274), then
         every micro-batch backward (gradients to the previous stage,
-        _send_gradient :276-297), then the optimizer step."""
+        _send_gradient :276-297), then the optimizer step.  `trace=True` keeps
+        this step's CUDA-event spans in `self.last_trace` (Chrome trace events,
+        pid = stage)."""
         s, S = self.s, self.S
         mbs, tgs = tokens.chunk(n_micro), targets.chunk(n_micro)
         pending, saved, losses = [], [], []
+        tl = _Timeline() if trace and self.device.type == "cuda" else None
+
+        def span(name, cat):
+            return tl.span(name, cat) if tl is not None else _NoSpan()
+
         for m in range(n_micro):  # fill
-            inp = mbs[m] if s == 0 else self._recv(s - 1, m, KIND_ACTIVATION).requires_grad_(True)
-            with self._amp():
+            with span(f"recv act mb{m}", "recv"):
+                inp = mbs[m] if s == 0 else self._recv(s - 1, m, KIND_ACTIVATION).requires_grad_(True)
+            with span(f"stage{s} mb{m}", "fp"), self._amp():
                 y = self.stage(inp, tgs[m] if s == S - 1 else None)
             saved.append((inp, y))
             if s < S - 1:
-                pending.append(self._send(y, s + 1, m, KIND_ACTIVATION))
+                with span(f"{s}->{s + 1} mb{m}", "send"):
+                    pending.append(self._send(y, s + 1, m, KIND_ACTIVATION))
                 self.messages.append(("fp", s, s + 1, m))
             else:
                 losses.append(y.detach())
         for m in range(n_micro):  # drain
             inp, y = saved[m]
             if s == S - 1:
-                (y / n_micro).backward()
+                with span(f"stage{s} mb{m}", "bp"):
+                    (y / n_micro).backward()
             else:
-                y.backward(self._recv(s + 1, m, KIND_GRADIENT))
+                with span(f"recv grad mb{m}", "recv"):
+                    g = self._recv(s + 1, m, KIND_GRADIENT)
+                with span(f"stage{s} mb{m}", "bp"):
+                    y.backward(g)
             if s > 0:
-                pending.append(self._send(inp.grad, s - 1, m, KIND_GRADIENT))
+                with span(f"{s}->{s - 1} mb{m}", "send"):
+                    pending.append(self._send(inp.grad, s - 1, m, KIND_GRADIENT))
                 self.messages.append(("bp", s, s - 1, m))
         for w, _buf in pending:
             w.wait()
-        self.opt.step()
-        self.opt.zero_grad(set_to_none=True)
+        with span(f"stage{s} optimizer", "opt"):
+            self.opt.step()
+            self.opt.zero_grad(set_to_none=True)
+        if tl is not None:
+            self.last_trace = tl.events(pid=s, tid=f"stage{s} (rank {self.rank})")
         loss = torch.stack(losses).mean() if losses else torch.zeros((), device=self.device)
         dist.broadcast(loss, self.chain[S - 1])
         self.step_no += 1
@@ -619,13 +677,27 @@ class DistPipeline:
 MODELS = {"small": GPT2_SMALL, "medium": GPT2_MEDIUM, "xl": GPT2_XL}
 
 
+def gather_chrome_trace(pipe: "DistPipeline") -> Optional[str]:
+    """Every rank's `last_trace` in one Chrome trace (the reference's format,
+    simulator.py:75-95); returned on every rank.  Ranks start their step clocks
+    at the barrier before the traced step, so the stages line up to within the
+    barrier's skew."""
+    import json
+
+    mine = getattr(pipe, "last_trace", [])
+    allv = [None] * dist.get_world_size()
+    dist.all_gather_object(allv, mine)
+    events = [e for v in allv for e in (v or [])]
+    return json.dumps({"traceEvents": events, "displayTimeUnit": "ms"}, sort_keys=True)
+
+
 def _stage_links(S: int) -> list:
     return [(s, s + 1) for s in range(S - 1)] + [(s + 1, s) for s in range(S - 1)]
 
 
 def run_pipeline(model: str = "medium", plan_mode: str = "uniform", ratio: float = 100.0, micro_batch: int = None,
                  n_micro: int = None, seq_len: int = 1024, steps: int = 3, warmup: int = 1, codec=None,
-                 codec_name: str = "sm_100a FrameCodec") -> dict:
+                 codec_name: str = "sm_100a FrameCodec", trace_path=None) -> dict:
     """Time GPipe steps of GPT-2 with one stage per rank (or one stage on one GPU).
 
     plan_mode:
@@ -685,6 +757,19 @@ def run_pipeline(model: str = "medium", plan_mode: str = "uniform", ratio: float
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         times = tt.tolist()
     t = sorted(times)[len(times) // 2]  # median step
+    trace_file = None
+    if trace_path and world > 1:  # one more step with CUDA-event spans, as a Chrome trace
+        tok, tgt = synthetic_batch(cfg, gb, seq_len, dev, seed=warmup + steps)
+        dist.barrier()
+        torch.cuda.synchronize()
+        pipe.step(tok, tgt, n_micro, trace=True)
+        doc = gather_chrome_trace(pipe)
+        if dist.get_rank() == 0:
+            import pathlib
+
+            pathlib.Path(trace_path).parent.mkdir(parents=True, exist_ok=True)
+            pathlib.Path(trace_path).write_text(doc)
+        trace_file = str(trace_path)
     links = {}
     if dev_plan is not None:
         ks, rs = dev_plan.k.tolist(), dev_plan.r.tolist()
@@ -713,7 +798,7 @@ def run_pipeline(model: str = "medium", plan_mode: str = "uniform", ratio: float
                                              "Eq. 6 + select_k on the device, k read by the kernels",
                                  "adatopk": "reference cli.cross_link_times over the simulated two-cluster "
                                             "network (alpha + beta*M per cross-device FP edge)"}.get(plan_mode),
-           "fp_model": model_check,
+           "fp_model": model_check, "trace": trace_file,
            "schedule": "GPipe fill-drain (executor.py:389-404), bf16 autocast, fp32 boundaries",
            "data": "synthetic tokens, random init"}
     if ofp is not None:

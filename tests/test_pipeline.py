@@ -188,9 +188,14 @@ def _dist_worker(rank, world, port, q, mode="nccl"):
         for i in range(3):
             tok, tgt = PL.synthetic_batch(PL.GPT2_TINY, 8, 64, dev, seed=i)
             losses.append(pipe.step(tok, tgt, n_micro=4))
+        # one more step with CUDA-event spans, gathered into one Chrome trace
+        tok, tgt = PL.synthetic_batch(PL.GPT2_TINY, 8, 64, dev, seed=9)
+        pipe.step(tok, tgt, n_micro=4, trace=True)
+        import json
+        trace = json.loads(PL.gather_chrome_trace(pipe))["traceEvents"]
         dist.barrier()
         dist.destroy_process_group()
-        q.put((rank, losses))
+        q.put((rank, losses if rank else (losses, trace)))
     except Exception as e:
         q.put((rank, repr(e)))
 
@@ -213,7 +218,13 @@ def test_dist_pipeline_matches_virtual(cuda, mode):
     res = dict(q.get(timeout=600) for _ in range(2))
     for p in ps:
         p.join(timeout=60)
-    assert isinstance(res[0], list), res
+    assert isinstance(res[0], tuple), res
+    res[0], trace = res[0]
+    # the measured step in the reference's Chrome trace format (simulator.py:75-95)
+    cats = {(e["pid"], e["cat"]) for e in trace}
+    assert {(0, "fp"), (0, "bp"), (0, "send"), (0, "recv"), (1, "fp"), (1, "bp"), (1, "send"), (1, "recv")} <= cats
+    assert all(e["ph"] == "X" and e["dur"] >= 0 and e["ts"] >= 0 for e in trace)
+    assert sum(1 for e in trace if e["pid"] == 0 and e["cat"] == "fp") == 4
     torch.use_deterministic_algorithms(True, warn_only=True)
     try:
         plan = PL.link_plan(2, "uniform", 10.0)
