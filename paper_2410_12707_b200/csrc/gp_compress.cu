@@ -65,6 +65,9 @@ constexpr uint32_t kFcCapBig = 65536;  // final candidates the fast path accepts
 #ifndef GP_DEFER_REST
 #define GP_DEFER_REST 1
 #endif
+#ifndef GP_GROUP_COPY
+#define GP_GROUP_COPY 0
+#endif
 #ifndef GP_SKIP_EMPTY
 #define GP_SKIP_EMPTY 0
 #endif
@@ -438,17 +441,29 @@ __global__ void __launch_bounds__(kCompressThreads, 1) compress_kernel(const Com
     bulk_load_async(ring + slot * 2048u, xw + (size_t)p * 512u, min(64u, nch - p * 64u) * 32u, mbar + slot * 8u,
                     policy);
   };
+#if GP_GROUP_COPY
+  // group mode: both ring slots (contiguous in smem) refilled by ONE 4 KiB
+  // copy of two consecutive row pairs, completing on slot 0's mbarrier
+  auto issue_group = [&](uint32_t g) {
+    bulk_load_async(ring, xw + (size_t)g * 1024u, min(128u, nch - g * 128u) * 32u, mbar, policy);
+  };
+#endif
   // the rest of the warp's opening requests: the other ring pairs and, for a
   // short unit, its remaining rows sent to L2 (no second HBM round trip)
   auto issue_rest = [&]() {
-    for (uint32_t p = 1; p < min(npair, kPairs); ++p) issue(p, p);
+    if (!GP_GROUP_COPY)
+      for (uint32_t p = 1; p < min(npair, kPairs); ++p) issue(p, p);
     if (nrow > kRing && nrow <= kRing + kPrefetchRows)
       prefetch_l2_bulk(xw + (size_t)kRing * 256u, (nch - kRing * 32u) * 32u);
   };
   if (lane == 0) {
     for (uint32_t s = 0; s < kPairs; ++s) mbar_init(mbar + s * 8u, 1u);
     fence_mbar_init();
+#if GP_GROUP_COPY
+    if (npair > 0) issue_group(0);
+#else
     if (npair > 0) issue(0, 0);
+#endif
     if (!GP_DEFER_REST) issue_rest();
   }
   __syncwarp();
@@ -573,7 +588,7 @@ __global__ void __launch_bounds__(kCompressThreads, 1) compress_kernel(const Com
 
   STAMP(1);
   if (GP_EXIT_AT == 1) {  // drain the ring first: no bulk copy may outlive the CTA
-    for (uint32_t p = 0; p < min(npair, kPairs); ++p) mbar_wait(mbar + p * 8u, 0u);
+    for (uint32_t p = 0; p < (GP_GROUP_COPY ? min(npair, 1u) : min(npair, kPairs)); ++p) mbar_wait(mbar + p * 8u, 0u);
     return;
   }
   uint32_t L = 0;                              // this warp's candidate count
@@ -749,6 +764,33 @@ __global__ void __launch_bounds__(kCompressThreads, 1) compress_kernel(const Com
       }
     };
     static_assert(kRing == 4, "two row-pair slots");
+#if GP_GROUP_COPY
+    const uint32_t q0 = seq;  // groups of two row pairs issued so far (mbarrier phases of slot 0)
+    const uint32_t ngroups = (npair + 1) / 2;
+    if (!preloaded && lane == 0 && npair > 0) {
+      fence_proxy_async_smem();
+      issue_group(0);
+    }
+    auto run_pairs = [&](auto all_c) {
+      const uint32_t nfull = nch / 64u;
+      for (uint32_t p = 0; p < npair; ++p) {
+        const uint32_t g = p >> 1, slot = p & 1u;
+        if (slot == 0) mbar_wait(mbar, (q0 + g) & 1u);
+        if (p < nfull) process2(2u * p, ring + slot * 2048u, ring + slot * 2048u + 1024u, std::true_type{}, all_c);
+        else process2(2u * p, ring + slot * 2048u, ring + slot * 2048u + 1024u, std::false_type{}, all_c);
+        if (slot == 1 || p + 1 == npair) {
+          __syncwarp();
+          if (lane == 0 && g + 1 < ngroups) {  // both slots consumed: refill them with the next group
+            fence_proxy_async_smem();
+            issue_group(g + 1);
+          }
+        }
+      }
+    };
+    if (all) run_pairs(std::true_type{});
+    else run_pairs(std::false_type{});
+    seq = q0 + ngroups;
+#else
     const uint32_t q0 = seq;
     if (!preloaded && lane == 0) {
       fence_proxy_async_smem();
@@ -771,6 +813,7 @@ __global__ void __launch_bounds__(kCompressThreads, 1) compress_kernel(const Com
     if (all) run_pairs(std::true_type{});
     else run_pairs(std::false_type{});
     seq = q0 + npair;
+#endif
     const Key span = lo ? Tr::kInfAbs - lo_m1 : ~(Key)0;
     for (uint32_t i0 = nch * EPL; i0 < n; i0 += 32u) {  // scalar tail / unaligned input
       const uint32_t i = i0 + lane;
