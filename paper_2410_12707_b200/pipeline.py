@@ -666,6 +666,11 @@ class DistPipeline:
         loss = torch.stack(losses).mean() if losses else torch.zeros((), device=self.device)
         dist.broadcast(loss, self.chain[S - 1])
         self.step_no += 1
+        if check and self.dev_plan is not None:
+            st = int(self.dev_plan.status.item())  # the on-device Eq. 6's status (InvalidRatio / NoCommunication)
+            if st:
+                from .errors import raise_for_status
+                raise_for_status(st, "gp_adatopk_plan")
         if check and hasattr(self.codec, "check"):
             self.codec.check()  # one flag read per step: a corrupt received frame raises here
         elif check and self._err is not None and int(self._err.item()):
