@@ -361,6 +361,12 @@ def run_ours(args, rank, world, local_rank):
     direct = peer and args.transport == "peer-store"
     pull = peer and args.transport == "peer-pull"
     ring = copy_streams = cpu_group = None
+    # diagnostic only (N=1): the N>1 copy pattern into a local buffer, to
+    # separate the copies' cost on this GPU from the peer's incoming writes
+    localcopy = world == 1 and os.environ.get("GP_BENCH_LOCALCOPY") == "1"
+    if localcopy:
+        copy_streams = [torch.cuda.Stream(dev) for _ in range(max(1, args.streams))]
+        lc_order = [i for lst in per_stream for i in lst]
     if peer:
         from paper_2410_12707_b200.peer import PeerRing
 
@@ -418,10 +424,19 @@ def run_ours(args, rank, world, local_rank):
             compress(u, ring.peer_recv(parity) + u["off"] if direct else ring.recv(parity) + u["off"] if pull else None)
             if ev is not None:
                 ev[i][1].record(st)
-            if peer and not direct and not pull:  # frame i travels while the next frames are being compressed
+            if (peer and not direct and not pull) or localcopy:  # frame i travels while the next frames are being compressed
                 done[i].record(st)
-        done = [torch.cuda.Event() for _ in units] if peer and not direct and not pull else None
+        done = [torch.cuda.Event() for _ in units] if (peer and not direct and not pull) or localcopy else None
         on_streams(body)
+        if localcopy:
+            for n_, i in enumerate(lc_order):
+                u = units[i]
+                cs = copy_streams[n_ % len(copy_streams)]
+                cs.wait_event(done[i])
+                assert L.gp_copy_async(u["rframe"].data_ptr(), u["frame"].data_ptr(), 16 + 12 * u["k"],
+                                       cs.cuda_stream) == 0
+            for cs in copy_streams:
+                torch.cuda.current_stream(dev).wait_stream(cs)
         if peer and not direct and not pull and not nocopy:
             # copies in the estimated order the frames complete, round-robin over the copy streams
             for n_, i in enumerate(copy_order):

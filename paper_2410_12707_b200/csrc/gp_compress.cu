@@ -79,6 +79,12 @@ constexpr int kWmFineBins = 4096;      // watermark refinement: fine sample bins
 #define GP_REFINE_MIN_ROWS 32
 #endif
 constexpr size_t kRefineMinUnitBytes = (size_t)GP_REFINE_MIN_ROWS * 1024;  // refine for units of >= this many rows
+#ifndef GP_LIST_EVICT_LAST
+#define GP_LIST_EVICT_LAST 0
+#endif
+#ifndef GP_LIST_DISCARD
+#define GP_LIST_DISCARD 1
+#endif
 #ifndef GP_PREFETCH_ROWS
 #define GP_PREFETCH_ROWS 8
 #endif
@@ -101,6 +107,21 @@ struct Entry {
     } else {
       reinterpret_cast<uint4*>(base)[pos] = make_uint4(idx, 0u, (uint32_t)b, (uint32_t)((uint64_t)b >> 32));
     }
+  }
+  // a spilled (global) entry: L2 evict_last (GP_LIST_EVICT_LAST), so the list
+  // survives other streams' normal-priority traffic until the walk
+  __device__ __forceinline__ static void put_glob(unsigned char* base, uint32_t pos, uint32_t idx,
+                                                  typename Tr::Bits b) {
+#if GP_LIST_EVICT_LAST
+    if constexpr (kBytes == 8) {
+      st_global_v2_hint(reinterpret_cast<uint2*>(base) + pos, idx, (uint32_t)b, l2_evict_last_policy());
+    } else {
+      st_global_v4_hint(reinterpret_cast<uint4*>(base) + pos,
+                        make_uint4(idx, 0u, (uint32_t)b, (uint32_t)((uint64_t)b >> 32)), l2_evict_last_policy());
+    }
+#else
+    put(base, pos, idx, b);
+#endif
   }
   // plain loads: global entries were written by this warp, and grid barriers
   // (acquire fences) separate any cross-SM producer
@@ -126,7 +147,18 @@ struct WarpList {
   unsigned char* glob;
   __device__ __forceinline__ void put(uint32_t j, uint32_t idx, typename Tr::Bits b) const {
     if (j < Entry<Tr>::kSmemCap) Entry<Tr>::put(smem, j, idx, b);
-    else Entry<Tr>::put(glob, j, idx, b);
+    else Entry<Tr>::put_glob(glob, j, idx, b);
+  }
+  // after the last pass over an L-entry list: its spilled lines are dead, drop
+  // them from L2 instead of writing them back (GP_LIST_DISCARD)
+  __device__ __forceinline__ void discard(uint32_t L) const {
+#if GP_LIST_DISCARD
+    constexpr uint32_t kB = Entry<Tr>::kBytes;
+    static_assert(Entry<Tr>::kSmemCap * kB % 128 == 0, "the global part starts on a line");
+    const uint32_t lane = threadIdx.x & 31;
+    for (uint32_t ln = Entry<Tr>::kSmemCap * kB / 128 + lane; ln < (L * kB + 127) / 128; ln += 32)
+      discard_l2_line(glob + (size_t)ln * 128);
+#endif
   }
   __device__ __forceinline__ void get(uint32_t j, uint32_t& idx, typename Tr::Bits& b) const {
     Entry<Tr>::get(j < Entry<Tr>::kSmemCap ? smem : glob, j, idx, b);
@@ -753,7 +785,7 @@ __global__ void __launch_bounds__(kCompressThreads, 1) compress_kernel(const Com
               const uint32_t e = __ffs(mm) - 1;
               mm &= mm - 1;
               const Bits bv = ld_shared_elem<Tr>(src + e * (uint32_t)sizeof(Elem));
-              if constexpr (decltype(glob_only)::value) Entry<Tr>::put(list.glob, pos[j]++, base + e, bv);
+              if constexpr (decltype(glob_only)::value) Entry<Tr>::put_glob(list.glob, pos[j]++, base + e, bv);
               else list.put(pos[j]++, base + e, bv);
             }
           }
@@ -1272,6 +1304,7 @@ __global__ void __launch_bounds__(kCompressThreads, 1) compress_kernel(const Com
     };
     if (a.idx64 && a.val_f32 && a.val2_out == nullptr) walk(std::true_type{});
     else walk(std::false_type{});
+    list.discard(L);
     }  // fast (no CTA overflowed)
   }
   if (!fast) {
@@ -1363,6 +1396,7 @@ __global__ void __launch_bounds__(kCompressThreads, 1) compress_kernel(const Com
       o += __popc(sm);
       er += __popc(em);
     });
+    list.discard(L);
     if (c == 0) {
       for (uint32_t i = tid; i < (uint32_t)(lvl * 256); i += kCompressThreads) a.hist_lvl[i] = 0u;
     }
