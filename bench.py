@@ -899,6 +899,34 @@ def bench_c1(P, L, dev, flush, peak, reps=20):
            "pair_us": round(c + dd, 2), "pair_gbs": round(b / ((c + dd) * 1e-6) / 1e9, 1),
            "frac_of_peak": round(b / ((c + dd) * 1e-6) / 1e9 / peak, 4),
            "note": "one tensor: per-launch CUDA events after a 512 MB L2 flush; includes launch latency"}
+    # warm (L2-flush vs warm): 100 pairs on the same tensor in one
+    # CUDA graph, no flush -- the input L2-resident, as right after the layer
+    # that produced it; per-pair time = graph time / 100
+    n_warm = 100
+    side = torch.cuda.Stream(dev)
+    side.wait_stream(torch.cuda.current_stream(dev))
+    gph = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(gph, stream=side):
+        sps = side.cuda_stream
+        for _ in range(n_warm):
+            L.gp_topk_compress_frame(x.data_ptr(), 0, d, k, frame.data_ptr(), ws.data_ptr(), wsb, sps)
+            L.gp_topk_decompress_frame(frame.data_ptr(), k, d, out.data_ptr(), 0, 2, err.data_ptr(), sps)
+    gph.replay()
+    torch.cuda.synchronize(dev)
+    tw = []
+    for _ in range(5):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        gph.replay()
+        e1.record()
+        e1.synchronize()
+        tw.append(e0.elapsed_time(e1) * 1e3 / n_warm)
+    w = statistics.median(tw)
+    res["warm_graph"] = {"pair_us": round(w, 2), "pair_gbs": round(b / (w * 1e-6) / 1e9, 1),
+                         "frac_of_peak": round(b / (w * 1e-6) / 1e9 / peak, 4),
+                         "note": f"{n_warm} compress+decompress pairs of the same tensor in one CUDA graph, no L2 "
+                                 "flush (input L2-resident, as right after the producing layer), median of 5 replays"}
+    assert int(err.item()) == 0
     # Throughput on GPT-2 activation shapes: the n_micro = 8 boundary tensors of
     # one pipeline flush in flight (the north star's
     # ">= 60% of the HBM roofline on GPT-2 activation shapes")
