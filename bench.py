@@ -940,7 +940,7 @@ def bench_c1(P, L, dev, flush, peak, reps=20):
         res[key] = {"shape": list(shape), "ratio": 100, "tensors": 8, "us": round(t, 2), "gbs": round(gbs, 1),
                     "frac_of_peak": round(gbs / peak, 4),
                     "note": "8 independent tensors (one pipeline flush of boundaries), compress then decompress "
-                            "each, 8 streams x 18-CTA grids (a workspace per stream), one CUDA graph, L2 flushed "
+                            "each, 8 streams x 19- and 18-CTA grids (all SMs; a workspace per stream), one CUDA graph, L2 flushed "
                             "(512 MB read) before each replay, median"}
     return res
 
@@ -957,7 +957,9 @@ def gpt2_batch(L, dev, shape, n, ns, flush, ratio=100.0, reps=10):
         d *= v
     k = select_k(d, ratio)
     wsb = L.gp_topk_workspace_bytes(d, 0)
-    ctas = max(1, torch.cuda.get_device_properties(dev).multi_processor_count // ns)
+    nsm = torch.cuda.get_device_properties(dev).multi_processor_count
+    ctas = max(1, nsm // ns)
+    ctas_of = [ctas + (1 if j < nsm % ns else 0) for j in range(ns)]  # every SM busy (148 = 4 x 19 + 4 x 18)
     xs = [torch.randn(d, device=dev, generator=g) for _ in range(n)]
     frames = [torch.empty(16 + 12 * k, dtype=torch.uint8, device=dev) for _ in range(n)]
     outs = [torch.empty(d, device=dev) for _ in range(n)]
@@ -975,7 +977,7 @@ def gpt2_batch(L, dev, shape, n, ns, flush, ratio=100.0, reps=10):
         for i in range(n):
             st = sts[i % ns]
             assert L.gp_topk_compress_frame_ctas(xs[i].data_ptr(), 0, d, k, frames[i].data_ptr(),
-                                                 wss[i % ns].data_ptr(), wsb, st.cuda_stream, ctas) == 0
+                                                 wss[i % ns].data_ptr(), wsb, st.cuda_stream, ctas_of[i % ns]) == 0
             assert L.gp_topk_decompress_frame(frames[i].data_ptr(), k, d, outs[i].data_ptr(), 0, 2, err.data_ptr(),
                                               st.cuda_stream) == 0
         for st in sts:
