@@ -244,20 +244,34 @@ class _Flags:
         return v
 
 
-def _as_device_flat(vector, device: torch.device) -> torch.Tensor:
-    """Flatten like `np.asarray(vector).reshape(-1)` (compressor.py:85-87), on the device."""
+def _compute_dtype(dtype: torch.dtype) -> torch.dtype:
+    """The kernel dtype an input dtype is ranked in: f32/bf16/f64 as they are,
+    float16 as float32 and integers/bool as float64 (exact widenings that keep
+    the magnitude order; integers exactly below 2^53)."""
+    if dtype in _DTYPE_CODE:
+        return dtype
+    if dtype.is_floating_point:
+        return torch.float32 if torch.finfo(dtype).bits <= 16 else torch.float64
+    if dtype.is_complex:
+        raise TypeError(f"unsupported dtype {dtype}")
+    return torch.float64
+
+
+def _as_device_flat(vector, device: torch.device):
+    """Flatten like `np.asarray(vector).reshape(-1)` (compressor.py:85-87), on
+    the device; returns (flat tensor in its kernel dtype, the input's dtype)."""
     if isinstance(vector, torch.Tensor):
         t = vector
     else:
-        arr = np.asarray(vector)
-        if arr.dtype.kind in "iub":
-            arr = arr.astype(np.float64)  # |int| < 2^53 ranks identically as float64
-        elif arr.dtype == np.float16:
-            arr = arr.astype(np.float32)  # exact widening, same order
-        t = torch.from_numpy(np.ascontiguousarray(arr))
+        t = torch.from_numpy(np.ascontiguousarray(np.asarray(vector)))
+    orig = t.dtype
     if t.device != device:
         t = t.to(device, non_blocking=t.is_pinned())
-    return t.reshape(-1).contiguous()
+    t = t.reshape(-1)
+    cd = _compute_dtype(orig)
+    if cd != orig:
+        t = t.to(cd)
+    return t.contiguous(), orig
 
 
 # ---------------------------------------------------------------------------
@@ -292,7 +306,7 @@ def topk_compress(vector, ratio: float, *, stream=None) -> SparsePayload:
 
 
 def _topk_compress_on(vector, ratio: float, device: torch.device) -> SparsePayload:
-    flat = _as_device_flat(vector, device)
+    flat, orig_dtype = _as_device_flat(vector, device)
     d = flat.numel()
     if d == 0:
         raise EmptyVector("cannot compress a zero-length vector")
@@ -310,6 +324,8 @@ def _topk_compress_on(vector, ratio: float, device: torch.device) -> SparsePaylo
         flat.data_ptr(), code, d, k, idx.data_ptr(), 8, fvals.data_ptr(), _lib.DTYPE_F32,
         None if code == _lib.DTYPE_F32 else values.data_ptr(), frame.data_ptr(), ws_ptr, ws_bytes, sp)
     raise_for_status(st, "gp_topk_compress", ratio)
+    if orig_dtype != values.dtype:  # the reference keeps the input dtype (values = flat[kept].copy())
+        values = values.to(orig_dtype)  # exact: every value came from an input of that dtype
     p = SparsePayload(values=values, indices=idx, original_len=d, frame=frame)
     p._produced = (idx, idx._version, values, values._version, d)
     p._kernel_made = True
@@ -348,13 +364,22 @@ def _topk_decompress_on(payload, device: torch.device, out, accumulate: bool, ch
     d, k = int(payload.original_len), int(values.numel())
     if indices.numel() != k:  # numpy raises on the shape mismatch in the reference (compressor.py:101-102)
         raise ValueError(f"payload has {k} values but {indices.numel()} indices")
-    code = _DTYPE_CODE.get(values.dtype)
-    if code is None:
-        raise TypeError(f"unsupported value dtype {values.dtype}")
-    if out is None:
-        out = (torch.zeros if accumulate else torch.empty)(d, dtype=values.dtype, device=device)
-    elif out.numel() != d or not out.is_contiguous():
+    # the output has the values' dtype (np.zeros(d, values.dtype)); dtypes the
+    # kernels do not take (integers, bool, float16) run widened and are cast back
+    # exactly at the end
+    user_out = out
+    if out is not None and (out.numel() != d or not out.is_contiguous()):
         raise ValueError("out must be a contiguous tensor of original_len elements")
+    res_dtype = values.dtype if out is None else out.dtype
+    if values.dtype not in _DTYPE_CODE:
+        values = values.to(_compute_dtype(values.dtype))
+    code = _DTYPE_CODE[values.dtype]
+    if out is None or out.dtype not in _DTYPE_CODE:
+        wd = values.dtype if out is None else _compute_dtype(out.dtype)
+        if accumulate:
+            out = torch.zeros(d, dtype=wd, device=device) if user_out is None else user_out.to(wd)
+        else:
+            out = torch.empty(d, dtype=wd, device=device)
     out_code = _DTYPE_CODE[out.dtype]
     if d == 0 and k > 0:
         raise IndexOutOfRange(indices)
@@ -382,6 +407,11 @@ def _topk_decompress_on(payload, device: torch.device, out, accumulate: bool, ch
             flag = _Flags.read(err)
         if flag & _lib.FLAG_OUT_OF_RANGE:
             raise IndexOutOfRange(indices)
+    if out.dtype != res_dtype:  # widened run: back to the values' (or the caller's out) dtype
+        if user_out is not None:
+            user_out.copy_(out)
+            return user_out
+        return out.to(res_dtype)
     return out
 
 

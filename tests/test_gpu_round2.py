@@ -323,3 +323,36 @@ def test_trusted_decompress_equals_checked(cuda, ratio):
     ref = torch.zeros_like(x)
     ref[p.indices] = x[p.indices]
     assert torch.equal(P.topk_decompress(p).view(torch.int32), ref.view(torch.int32))
+
+
+# --------------------------------------------------------------------------- input dtypes
+
+
+@pytest.mark.parametrize("dtype", [np.int64, np.int32, np.int16, np.float16])
+def test_input_dtype_is_kept_like_the_reference(cuda, dtype):
+    """values = flat[kept].copy() and np.zeros(d, values.dtype) keep the input
+    dtype in the reference (compressor.py:94,101): integer and float16 inputs
+    rank in an exact widening on the device and come back in their own dtype;
+    frames carry the same f32 wire values as the reference's astype('<f4')."""
+    rng = np.random.default_rng(5)
+    if dtype == np.float16:
+        x = rng.standard_normal(50_000).astype(np.float16)
+    else:  # many exact ties: the lower-index rule decides most of the kept set
+        x = rng.integers(-1000, 1000, size=50_000).astype(dtype)
+    for ratio in (10.0, 100.0):
+        p = P.topk_compress(x, ratio)
+        vals, idx, d = O.topk_compress(x, ratio, method="argsort")
+        assert p.values.dtype == torch.from_numpy(vals).dtype
+        assert np.array_equal(p.indices.cpu().numpy(), idx)
+        assert np.array_equal(p.values.cpu().numpy(), vals)
+        assert p.to_bytes() == O.to_bytes(vals, idx, d)
+        dense = P.topk_decompress(p)
+        ref = O.topk_decompress(vals, idx, d)
+        assert dense.dtype == torch.from_numpy(ref).dtype
+        assert np.array_equal(dense.cpu().numpy(), ref)
+        # the same through a CUDA tensor of that dtype, and a modified payload (repacked frame)
+        pt = P.topk_compress(torch.from_numpy(x).to(cuda), ratio)
+        assert pt.values.dtype == p.values.dtype and torch.equal(pt.indices, p.indices)
+        q = dataclasses.replace(pt, values=pt.values.clone())
+        assert q.to_bytes() == O.to_bytes(vals, idx, d)
+        assert torch.equal(P.topk_decompress(q), dense)
