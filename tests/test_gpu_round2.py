@@ -356,3 +356,24 @@ def test_input_dtype_is_kept_like_the_reference(cuda, dtype):
         q = dataclasses.replace(pt, values=pt.values.clone())
         assert q.to_bytes() == O.to_bytes(vals, idx, d)
         assert torch.equal(P.topk_decompress(q), dense)
+
+
+def test_fp64_nan_payload_in_frames(cuda):
+    """kept fp64 NaNs reach the f32 wire value as NaN (the payload
+    bits may differ from numpy's astype('<f4')); indices and every non-NaN
+    value are bit-exact, and the decompressed fp64 vector keeps the input bits."""
+    x = np.array([1.5, np.nan, -2.25, 0.0, 3.0, -np.inf, 7.0, np.nan], dtype=np.float64)
+    x.view(np.uint64)[1] = 0x7FF8_0000_DEAD_BEEF  # quiet NaN with a payload
+    x.view(np.uint64)[7] = 0xFFF4_0000_0000_0001  # negative signalling-pattern NaN
+    for ratio in (1.0, 8.0 / 7.0, 2.0):
+        p = P.topk_compress(torch.from_numpy(x).to(cuda), ratio)
+        vals, idx, d = O.topk_compress(x, ratio, method="argsort")
+        assert np.array_equal(p.indices.cpu().numpy(), idx)
+        assert np.array_equal(p.values.cpu().numpy().view(np.uint64), vals.view(np.uint64))  # fp64 values: exact
+        got = np.frombuffer(p.to_bytes(), dtype="<f4", offset=16 + 8 * len(idx))
+        ref = vals.astype("<f4")
+        nan = np.isnan(ref)
+        assert np.array_equal(np.isnan(got), nan)
+        assert np.array_equal(got[~nan].view(np.uint32), ref[~nan].view(np.uint32))
+        dense = P.topk_decompress(p).cpu().numpy()
+        assert np.array_equal(dense.view(np.uint64), O.topk_decompress(vals, idx, d).view(np.uint64))
