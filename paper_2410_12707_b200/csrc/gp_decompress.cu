@@ -38,6 +38,14 @@ namespace gp {
 #define GP_DEC_BLOCKS_PER_SM 4
 #endif
 constexpr int kDecThreads = 512;
+#ifndef GP_DEC_PROBES
+#define GP_DEC_PROBES 128  // 512 before: -7 MB of probe reads per 205 MB r = 10 decompress, +1% (A/B)
+#endif
+// threads probing for a CTA's first entry: the probe window spans +-3 sigma of
+// a uniform spread around the interpolation guess; its stride must stay below
+// a batch (kDecThreads) so that the first batch brackets the entry
+constexpr int kProbes = GP_DEC_PROBES;
+static_assert(kProbes <= kDecThreads && kProbes % 32 == 0, "probes are whole warps of the CTA");
 constexpr int kDecBlocksPerSm = GP_DEC_BLOCKS_PER_SM;
 constexpr int kTileBytes = GP_DEC_TILE_KB * 1024;   // smem output tile
 #ifndef GP_DEC_EVICT_FIRST
@@ -231,22 +239,21 @@ __global__ void __launch_bounds__(kDecThreads, kDecBlocksPerSm) decompress_kerne
   // 2 loads the batch starting at the bracket.  Clustered indices that the
   // probe window misses fall back to a 32-ary search.
   const int64_t guess = d ? (int64_t)((double)k * (double)o0 / (double)d) : 0;  // a guess; rounding is harmless
-  const int64_t stride = max((int64_t)1, (int64_t)(3.0f * sqrtf((float)k) / kDecThreads) + 1);
+  const int64_t stride = max((int64_t)1, (int64_t)(3.0f * sqrtf((float)k) / kProbes) + 1);
   auto probe_pos = [&](int64_t t) {
-    const int64_t p = guess + (t - kDecThreads / 2) * stride;
+    const int64_t p = guess + (t - kProbes / 2) * stride;
     return p < 0 ? (int64_t)0 : (p >= k ? k - 1 : p);
   };
   int64_t base = 0;
   if (k > 0) {
-    const int64_t p = probe_pos(tid);
-    const int64_t pv = (int64_t)__ldg(idx + p);
+    const int64_t pv = tid < (uint32_t)kProbes ? (int64_t)__ldg(idx + probe_pos(tid)) : 0;
     // consume the early loads here (not at the end, where the compiler would
     // otherwise sink them into an extra serialized round trip)
     if (!(pa < pz)) bad = true;
     if (blockIdx.x == 0 && tid == 0 && (first < 0 || last >= d)) atomicOr(err, kFlagOutOfRange);
-    const int below = __syncthreads_count(pv < o0);
-    const int64_t p_first = probe_pos(0), p_last = probe_pos(kDecThreads - 1);
-    if ((below == 0 && p_first > 0) || (below == kDecThreads && p_last < k - 1)) {
+    const int below = __syncthreads_count(tid < (uint32_t)kProbes && pv < o0);
+    const int64_t p_first = probe_pos(0), p_last = probe_pos(kProbes - 1);
+    if ((below == 0 && p_first > 0) || (below == kProbes && p_last < k - 1)) {
       if (tid < 32) {  // probe window missed (clustered indices)
         const int64_t r = warp_lower_bound(idx, k, o0, guess);
         if (lane == 0) sh_lo = r;
@@ -373,13 +380,13 @@ __global__ void __launch_bounds__(kDecThreads, kDecBlocksPerSm) decompress_spars
     last = (int64_t)__ldg(idx + k - 1);
   }
   const int64_t guess = d ? (int64_t)((double)k * (double)o0 / (double)d) : 0;
-  const int64_t stride = max((int64_t)1, (int64_t)(3.0f * sqrtf((float)k) / kDecThreads) + 1);
+  const int64_t stride = max((int64_t)1, (int64_t)(3.0f * sqrtf((float)k) / kProbes) + 1);
   auto probe_pos = [&](int64_t t) {
-    const int64_t p = guess + (t - kDecThreads / 2) * stride;
+    const int64_t p = guess + (t - kProbes / 2) * stride;
     return p < 0 ? (int64_t)0 : (p >= k ? k - 1 : p);
   };
   int64_t pv = 0;
-  if (k > 0) pv = (int64_t)__ldg(idx + probe_pos(tid));
+  if (k > 0 && tid < (uint32_t)kProbes) pv = (int64_t)__ldg(idx + probe_pos(tid));
   // zero fill of the whole range while the probes are in flight
   if (((uintptr_t)(out + o0) % 16) == 0) {
     constexpr int V = 16 / (int)sizeof(OT);
@@ -394,10 +401,10 @@ __global__ void __launch_bounds__(kDecThreads, kDecBlocksPerSm) decompress_spars
   if (!(pa < pz)) bad = true;
   if (blockIdx.x == 0 && tid == 0 && (first < 0 || last >= d)) atomicOr(err, kFlagOutOfRange);
   __shared__ int64_t sh_lo;
-  const int below = __syncthreads_count(pv < o0);  // also orders the fill before the scatter
+  const int below = __syncthreads_count(tid < (uint32_t)kProbes && pv < o0);  // also orders the fill before the scatter
   int64_t base;
-  const int64_t p_first = probe_pos(0), p_last = probe_pos(kDecThreads - 1);
-  if ((below == 0 && p_first > 0) || (below == kDecThreads && p_last < k - 1)) {
+  const int64_t p_first = probe_pos(0), p_last = probe_pos(kProbes - 1);
+  if ((below == 0 && p_first > 0) || (below == kProbes && p_last < k - 1)) {
     if (tid < 32) {  // probe window missed (clustered indices)
       const int64_t r = warp_lower_bound(idx, k, o0, guess);
       if ((tid & 31) == 0) sh_lo = r;
