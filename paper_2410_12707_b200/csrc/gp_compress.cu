@@ -85,6 +85,9 @@ constexpr size_t kRefineMinUnitBytes = (size_t)GP_REFINE_MIN_ROWS * 1024;  // re
 #ifndef GP_LIST_DISCARD
 #define GP_LIST_DISCARD 1
 #endif
+#ifndef GP_LDGSTS
+#define GP_LDGSTS 1  // ring filled by per-lane cp.async (1) or by one bulk (TMA) copy per row pair (0)
+#endif
 #ifndef GP_PREFETCH_ROWS
 #define GP_PREFETCH_ROWS 8
 #endif
@@ -468,11 +471,31 @@ __global__ void __launch_bounds__(kCompressThreads, 1) compress_kernel(const Com
   const uint32_t mbar = smem_addr(smem + SL::mbar) + w * (kRing * 8u);
   const uint64_t policy = l2_evict_first_policy();  // x is read once: keep L2 for the lists
   uint32_t seq = 0;                                 // row pairs this warp has issued into the ring
+#if GP_LDGSTS
+  static_assert(!GP_GROUP_COPY, "cp.async ring: one row pair per commit group");
+  // every lane: the four 16-byte pieces of row pair p it reads itself (piece
+  // j*32 + lane of the pair), one commit group per call; rings are only ever
+  // read by the lane that filled the piece, so a per-thread wait is the only
+  // synchronisation (A/B on B200: a bulk copy per warp and row pair streams at
+  // ~25-40 GB/s per SM, per-lane cp.async at up to 150, scripts/layout_probe.cu)
+  auto issue = [&](uint32_t p, uint32_t q) {
+    const uint32_t slot = q % kPairs;
+    const uint32_t nb = min(64u, nch - p * 64u) * 32u;  // valid bytes of the pair
+    const unsigned char* src = reinterpret_cast<const unsigned char*>(xw + (size_t)p * 512u);
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const uint32_t o = (uint32_t)j * 512u + lane * 16u;
+      if (o < nb) cp_async16_hint(ring + slot * 2048u + o, src + o, policy);
+    }
+    cp_async_commit();
+  };
+#else
   auto issue = [&](uint32_t p, uint32_t q) {        // lane 0: row pair p as ring sequence number q
     const uint32_t slot = q % kPairs;
     bulk_load_async(ring + slot * 2048u, xw + (size_t)p * 512u, min(64u, nch - p * 64u) * 32u, mbar + slot * 8u,
                     policy);
   };
+#endif
 #if GP_GROUP_COPY
   // group mode: both ring slots (contiguous in smem) refilled by ONE 4 KiB
   // copy of two consecutive row pairs, completing on slot 0's mbarrier
@@ -483,12 +506,27 @@ __global__ void __launch_bounds__(kCompressThreads, 1) compress_kernel(const Com
   // the rest of the warp's opening requests: the other ring pairs and, for a
   // short unit, its remaining rows sent to L2 (no second HBM round trip)
   auto issue_rest = [&]() {
+#if GP_LDGSTS
+    for (uint32_t p = 1; p < kPairs; ++p) {  // every lane; one group per slot, empty past the unit
+      if (p < npair) issue(p, p);
+      else cp_async_commit();
+    }
+    if (lane == 0 && nrow > kRing && nrow <= kRing + kPrefetchRows)
+      prefetch_l2_bulk(xw + (size_t)kRing * 256u, (nch - kRing * 32u) * 32u);
+#else
     if (!GP_GROUP_COPY)
       for (uint32_t p = 1; p < min(npair, kPairs); ++p) issue(p, p);
     if (nrow > kRing && nrow <= kRing + kPrefetchRows)
       prefetch_l2_bulk(xw + (size_t)kRing * 256u, (nch - kRing * 32u) * 32u);
+#endif
   };
+#if GP_LDGSTS
+  if (npair > 0) issue(0, 0);
+  if (!GP_DEFER_REST) issue_rest();
+  if (false) {
+#else
   if (lane == 0) {
+#endif
     for (uint32_t s = 0; s < kPairs; ++s) mbar_init(mbar + s * 8u, 1u);
     fence_mbar_init();
 #if GP_GROUP_COPY
@@ -513,11 +551,20 @@ __global__ void __launch_bounds__(kCompressThreads, 1) compress_kernel(const Com
   if (tid < 32) sh_res[tid] = 0u;
   __syncthreads();
   if (nrow > 0) {
+#if GP_LDGSTS
+    if (GP_DEFER_REST) cp_async_wait<0>();  // row pair 0 (the only group so far)
+    else cp_async_wait<kPairs - 1>();
+    // deferred: the watermark needs only row pair 0 of every warp, so the
+    // rest of the unit is requested once this warp's pair 0 is in (it then
+    // streams in under the watermark's barriers instead of ahead of row 0s)
+    if (GP_DEFER_REST) issue_rest();
+#else
     mbar_wait(mbar, 0u);  // row pair 0
     // deferred: the watermark needs only row pair 0 of every warp, so the
     // rest of the unit is requested once this warp's pair 0 is in (it then
     // streams in under the watermark's barriers instead of ahead of row 0s)
     if (GP_DEFER_REST && lane == 0) issue_rest();
+#endif
     uint32_t ns = 0, mb = 0;
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
@@ -620,7 +667,11 @@ __global__ void __launch_bounds__(kCompressThreads, 1) compress_kernel(const Com
 
   STAMP(1);
   if (GP_EXIT_AT == 1) {  // drain the ring first: no bulk copy may outlive the CTA
+#if GP_LDGSTS
+    cp_async_wait<0>();
+#else
     for (uint32_t p = 0; p < (GP_GROUP_COPY ? min(npair, 1u) : min(npair, kPairs)); ++p) mbar_wait(mbar + p * 8u, 0u);
+#endif
     return;
   }
   uint32_t L = 0;                              // this warp's candidate count
@@ -824,22 +875,40 @@ __global__ void __launch_bounds__(kCompressThreads, 1) compress_kernel(const Com
     seq = q0 + ngroups;
 #else
     const uint32_t q0 = seq;
+#if GP_LDGSTS
+    if (!preloaded) {  // every lane: kPairs groups, empty past the unit
+      for (uint32_t p = 0; p < kPairs; ++p) {
+        if (p < npair) issue(p, q0 + p);
+        else cp_async_commit();
+      }
+    }
+#else
     if (!preloaded && lane == 0) {
       fence_proxy_async_smem();
       for (uint32_t p = 0; p < min(npair, kPairs); ++p) issue(p, q0 + p);
     }
+#endif
     auto run_pairs = [&](auto all_c) {
       const uint32_t nfull = nch / 64u;  // row pairs with both rows complete
       for (uint32_t p = 0; p < npair; ++p) {
         const uint32_t q = q0 + p, slot = q % kPairs;
+#if GP_LDGSTS
+        cp_async_wait<kPairs - 1>();  // exactly kPairs - 1 groups were committed after this pair's
+#else
         mbar_wait(mbar + slot * 8u, (q / kPairs) & 1u);
+#endif
         if (p < nfull) process2(2u * p, ring + slot * 2048u, ring + slot * 2048u + 1024u, std::true_type{}, all_c);
         else process2(2u * p, ring + slot * 2048u, ring + slot * 2048u + 1024u, std::false_type{}, all_c);
         __syncwarp();
+#if GP_LDGSTS
+        if (p + kPairs < npair) issue(p + kPairs, q + kPairs);  // refill the slot just consumed (every lane)
+        else cp_async_commit();  // an empty group keeps the wait count exact
+#else
         if (lane == 0 && p + kPairs < npair) {  // refill the slot just consumed
           fence_proxy_async_smem();
           issue(p + kPairs, q + kPairs);
         }
+#endif
       }
     };
     if (all) run_pairs(std::true_type{});
