@@ -49,10 +49,12 @@ def load(src):
     return [(names[i], launches[i]) for i in sorted(launches)]
 
 
-def bench_order(nstreams=6, dense_w=2.2, ovh=4e6, stagger=True):
+def bench_order(nstreams=5, dense_w=3.0, ovh=4e6, stagger=True, num_sms=148):
     """The units in the order bench.py captures them into its graphs (N=1): longest-first
-    greedy assignment to streams by its cost model, odd streams reversed, streams concatenated."""
+    greedy assignment to streams by its cost model (weighted by each stream's grid size),
+    odd streams reversed, streams concatenated."""
     us = units()
+    ctas_of = [num_sms // nstreams + (1 if j < num_sms % nstreams else 0) for j in range(nstreams)]
 
     def cost(u):
         return u[3] * (dense_w if u[2] <= 10 else 1.0) + ovh
@@ -62,7 +64,7 @@ def bench_order(nstreams=6, dense_w=2.2, ovh=4e6, stagger=True):
     for i in sorted(range(len(us)), key=lambda i: -cost(us[i])):
         j = min(range(nstreams), key=lambda j: load[j])
         per[j].append(i)
-        load[j] += cost(us[i])
+        load[j] += cost(us[i]) * ctas_of[0] / ctas_of[j]
     if stagger:
         for j in range(1, nstreams, 2):
             per[j].reverse()
