@@ -4,7 +4,7 @@
         profiles/ncu_launches_r02.md profiles/ncu_traffic.json
 
 The kernels are the 24 compress and 24 decompress nodes of one CUDA-graph
-replay in the bench's timed configuration (6 streams, 24-CTA compress grids,
+replay in the bench's timed configuration (5 streams, 30/29-CTA compress grids,
 24 distinct inputs).  ncu serialises the nodes, so each launch's time is
 cold-ish and alone; the units are matched to launches by their DRAM bytes
 (compress reads ~4d and writes the 16 + 12k frame; decompress writes ~4d).
@@ -123,7 +123,7 @@ def main(csv_c, csv_d, md_out, json_out):
         f.write("# ncu launch list, one timed bench step (round 2: the timed configuration)\n\n"
                 "`ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none` "
                 "over `bench.py --no-pipeline --no-sweep --steps 1 --warmup 3` with `GP_BENCH_SPINUP=0`: the 24 "
-                "compress and 24 decompress kernel nodes of the first timed CUDA-graph replay (6 streams, 24-CTA "
+                "compress and 24 decompress kernel nodes of the first timed CUDA-graph replay (5 streams, 30/29-CTA "
                 "compress grids, 24 distinct inputs; `scripts/gpu_ncu_r2.sh`).  ncu serialises the nodes: compare "
                 "shares and DRAM bytes, not absolute times.\n\n")
         f.write("\n".join(lines))
@@ -131,7 +131,7 @@ def main(csv_c, csv_d, md_out, json_out):
     json.dump({"compress_dram_bytes_per_launch_workload": tot["c_dram"] / max(1, n),
                "compress_alg_bytes_per_launch_workload": tot["c_alg"] / max(1, n),
                "decompress_dram_bytes_per_launch_workload": tot["d_dram"] / max(1, len(dec)),
-               "measured_on": "the timed configuration: 6 streams, CUDA-graph replay, 24 distinct inputs "
+               "measured_on": "the timed configuration: 5 streams, CUDA-graph replay, 24 distinct inputs "
                               "(ncu serialises the nodes)",
                "source": [csv_c, csv_d]}, open(json_out, "w"), indent=1)
     print(summary)
