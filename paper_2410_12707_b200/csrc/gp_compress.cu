@@ -88,6 +88,9 @@ constexpr size_t kRefineMinUnitBytes = (size_t)GP_REFINE_MIN_ROWS * 1024;  // re
 #ifndef GP_LDGSTS
 #define GP_LDGSTS 1  // ring filled by per-lane cp.async (1) or by one bulk (TMA) copy per row pair (0)
 #endif
+#ifndef GP_ISSUE_FULL
+#define GP_ISSUE_FULL 1  // full row pairs refilled without per-piece bounds
+#endif
 #ifndef GP_PREFETCH_ROWS
 #define GP_PREFETCH_ROWS 8
 #endif
@@ -490,6 +493,15 @@ __global__ void __launch_bounds__(kCompressThreads, 1) compress_kernel(const Com
       const uint32_t o = (uint32_t)j * 512u + lane * 16u;
       if (o < nb) cp_async16_hint(ring + slot * 2048u + o, src + o, policy);
     }
+    cp_async_commit();
+  };
+  // the same for a pair with all 64 chunks (the stream loop's case): one
+  // source pointer, immediate offsets, no per-piece bounds
+  auto issue_full = [&](uint32_t p, uint32_t q) {
+    const uint32_t d0 = ring + (q % kPairs) * 2048u + lane * 16u;
+    const unsigned char* s0 = reinterpret_cast<const unsigned char*>(xw + (size_t)p * 512u) + lane * 16u;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) cp_async16_hint(d0 + (uint32_t)j * 512u, s0 + j * 512, policy);
     cp_async_commit();
   };
 #else
@@ -904,8 +916,11 @@ __global__ void __launch_bounds__(kCompressThreads, 1) compress_kernel(const Com
         else process2(2u * p, ring + slot * 2048u, ring + slot * 2048u + 1024u, std::false_type{}, all_c);
         __syncwarp();
 #if GP_LDGSTS
-        if (p + kPairs < npair) issue(p + kPairs, q + kPairs);  // refill the slot just consumed (every lane)
-        else cp_async_commit();  // an empty group keeps the wait count exact
+        // refill the slot just consumed (every lane); an empty group past the
+        // unit keeps the wait count exact
+        if (GP_ISSUE_FULL && p + kPairs < nfull) issue_full(p + kPairs, q + kPairs);
+        else if (p + kPairs < npair) issue(p + kPairs, q + kPairs);
+        else cp_async_commit();
 #else
         if (lane == 0 && p + kPairs < npair) {  // refill the slot just consumed
           fence_proxy_async_smem();
