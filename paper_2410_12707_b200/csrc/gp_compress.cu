@@ -791,8 +791,6 @@ __global__ void __launch_bounds__(kCompressThreads, 1) compress_kernel(const Com
       // holds at most 32*EPS <= 128 candidates (f32, f64), else 16-bit fields
       constexpr int kField = EPS * 32 < 256 ? 8 : 16;
       using Packed = typename std::conditional<kField == 8, uint32_t, uint64_t>::type;
-      const Packed packed = (Packed)__popc(m[0]) | ((Packed)__popc(m[1]) << kField) |
-                            ((Packed)__popc(m[2]) << (2 * kField)) | ((Packed)__popc(m[3]) << (3 * kField));
       // sparse step (the common case above r ~ 50): no lane holds two
       // candidates in one sub-row, so ballots give every position directly and
       // each candidate is histogrammed where it is appended
@@ -816,7 +814,10 @@ __global__ void __launch_bounds__(kCompressThreads, 1) compress_kernel(const Com
         }
         return;
       }
-      if (__any_sync(kFull, packed != 0)) {
+      if (__any_sync(kFull, (m[0] | m[1] | m[2] | m[3]) != 0u)) {
+        // (built only here: the sparse steps above never need the counts)
+        const Packed packed = (Packed)__popc(m[0]) | ((Packed)__popc(m[1]) << kField) |
+                              ((Packed)__popc(m[2]) << (2 * kField)) | ((Packed)__popc(m[3]) << (3 * kField));
         Packed incl;
         if constexpr (kField == 8) incl = warp_incl_scan(packed);
         else incl = warp_incl_scan64(packed);
