@@ -4,7 +4,7 @@
         profiles/ncu_launches_r02.md profiles/ncu_traffic.json
 
 The kernels are the 24 compress and 24 decompress nodes of one CUDA-graph
-replay in the bench's timed configuration (5 streams, 30/29-CTA compress grids,
+replay in the bench's timed configuration (7 streams, 22/21-CTA compress grids,
 24 distinct inputs).  ncu serialises the nodes, so each launch's time is
 cold-ish and alone; the units are matched to launches by their DRAM bytes
 (compress reads ~4d and writes the 16 + 12k frame; decompress writes ~4d).
@@ -49,7 +49,7 @@ def load(src):
     return [(names[i], launches[i]) for i in sorted(launches)]
 
 
-def bench_order(nstreams=5, dense_w=3.0, ovh=4e6, stagger=True, num_sms=148):
+def bench_order(nstreams=7, dense_w=3.0, ovh=4e6, stagger=True, num_sms=148):
     """The units in the order bench.py captures them into its graphs (N=1): longest-first
     greedy assignment to streams by its cost model (weighted by each stream's grid size),
     odd streams reversed, streams concatenated."""
@@ -131,7 +131,7 @@ def main(csv_c, csv_d, md_out, json_out):
     json.dump({"compress_dram_bytes_per_launch_workload": tot["c_dram"] / max(1, n),
                "compress_alg_bytes_per_launch_workload": tot["c_alg"] / max(1, n),
                "decompress_dram_bytes_per_launch_workload": tot["d_dram"] / max(1, len(dec)),
-               "measured_on": "the timed configuration: 5 streams, CUDA-graph replay, 24 distinct inputs "
+               "measured_on": "the timed configuration: 7 streams, CUDA-graph replay, 24 distinct inputs "
                               "(ncu serialises the nodes)",
                "source": [csv_c, csv_d]}, open(json_out, "w"), indent=1)
     print(summary)
