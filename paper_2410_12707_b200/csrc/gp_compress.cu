@@ -12,8 +12,8 @@
 // vector is split into G*32 contiguous "units", one per warp, in index order,
 // so that a warp-ordered compaction of every unit concatenated in unit order
 // is globally index ordered.  A unit streams through a per-warp shared-memory
-// ring of two 2 KiB row-pair slots filled by bulk (TMA) copies, one mbarrier
-// per slot; each lane tests two 16-byte pieces of every row.
+// ring of two 2 KiB row-pair slots; each lane fills (cp.async) and tests the
+// two 16-byte pieces of every row it owns.
 //
 //   stage 0  each CTA takes a low watermark lo0 from a sample of its warps'
 //            first rows (4 keys per lane, no extra traffic): the key whose
