@@ -390,6 +390,15 @@ def run_ours(args, rank, world, local_rank):
                 acc += cost(units[i])
                 est_end[i] = acc
         copy_order = sorted(range(len(units)), key=lambda i: est_end[i])
+    # per-frame hand-off (N>1 push transport): each frame's copy records its
+    # own interprocess event, and the successor decompresses that unit as soon
+    # as its frame has landed -- the decompress phase overlaps the compress tail
+    # and the remaining copies instead of waiting for the last frame
+    frame_handoff = (peer and not direct and not pull and world > 1
+                     and os.environ.get("GP_BENCH_FRAME_HANDOFF", "1") == "1")
+    stream_d = torch.cuda.Stream(dev) if frame_handoff else None
+    if frame_handoff:
+        ring.enable_frame_events(len(units), cpu_group)
 
     def exchange():
         nxt, prv = (rank + 1) % world, (rank - 1) % world
@@ -401,19 +410,22 @@ def run_ours(args, rank, world, local_rank):
             w.wait()
 
     extra_streams = [torch.cuda.Stream(dev) for _ in range(nstreams - 1)]
+    # the decompress phase's own streams when it may overlap the compress phase
+    extra_streams_d = [torch.cuda.Stream(dev) for _ in range(nstreams - 1)] if frame_handoff else extra_streams
 
-    def on_streams(body):
+    def on_streams(body, extra=None):
         """Run body(i, u, st) for every unit on its stream: fork from, and join back into, the current stream."""
+        extra = extra_streams if extra is None else extra
         cur = torch.cuda.current_stream(dev)
-        sts = [cur] + extra_streams
-        for s_ in extra_streams:
+        sts = [cur] + extra
+        for s_ in extra:
             s_.wait_stream(cur)
         for i in stream_order:
             u = units[i]
             st = sts[u["sj"]]
             with torch.cuda.stream(st):
                 body(i, u, st)
-        for s_ in extra_streams:
+        for s_ in extra:
             cur.wait_stream(s_)
 
     # diagnostic only: skip the frame copies (the receive buffers keep the
@@ -448,6 +460,8 @@ def run_ours(args, rank, world, local_rank):
                 cs = copy_streams[n_ % len(copy_streams)]
                 cs.wait_event(done[i])
                 ring.copy(ring.peer_recv(parity) + u["off"], u["frame"].data_ptr(), 16 + 12 * u["k"], cs)
+                if frame_handoff:
+                    ring.signal_frame_sent(parity, i, cs)
             for cs in copy_streams:
                 torch.cuda.current_stream(dev).wait_stream(cs)
 
@@ -459,14 +473,18 @@ def run_ours(args, rank, world, local_rank):
                 src = (ring.peer_recv(parity) if pull else ring.recv(parity)) + u["off"]
             else:
                 src = (u["rframe"] if world > 1 else u["frame"]).data_ptr()
+            if frame_handoff:
+                ring.wait_frame_sent(parity, i, st)  # this unit's frame has landed
             decompress(u, src)
             if ev is not None:
                 ev[i][3].record(st)
-        on_streams(body)
+        on_streams(body, extra_streams_d)
 
     def handoff():
         """Between the compress and decompress phases of a step (N>1)."""
-        if peer:
+        if frame_handoff:  # every rank has enqueued this step's frame records (CPU only)
+            dist.barrier(group=cpu_group)
+        elif peer:
             ring.signal_sent(stream)
             dist.barrier(group=cpu_group)  # every rank has recorded its 'sent' event (CPU only)
             ring.wait_sent(stream)
@@ -478,11 +496,19 @@ def run_ours(args, rank, world, local_rank):
     def step(ev=None):
         p = parity[0]
         parity[0] ^= 1
+        if frame_handoff:  # the previous step's decompresses first (no overlap across steps)
+            stream.wait_stream(stream_d)
         if peer:
             ring.wait_consumed(stream)
         compress_all(ev, p)
         if world > 1:
             handoff()
+        if frame_handoff:
+            with torch.cuda.stream(stream_d):
+                decompress_all(ev, p)
+                ring.signal_consumed(stream_d)
+            stream.wait_stream(stream_d)
+            return
         decompress_all(ev, p)
         if peer:
             ring.signal_consumed(stream)
@@ -516,6 +542,8 @@ def run_ours(args, rank, world, local_rank):
         """One step; `mid` = (event after the compress launches, event before the decompress launches)."""
         p = parity[0] if peer else 0
         parity[0] ^= 1
+        if frame_handoff:
+            stream.wait_stream(stream_d)
         if peer:
             ring.wait_consumed(stream)
         if graphs is None:
@@ -526,6 +554,19 @@ def run_ours(args, rank, world, local_rank):
             mid[0].record(stream)
         if world > 1:
             handoff()
+        if frame_handoff:
+            # the decompress graph on its own stream: it waits only for the
+            # predecessor's per-frame events, not for this rank's compresses
+            with torch.cuda.stream(stream_d):
+                if mid is not None:
+                    mid[1].record(stream_d)
+                if graphs is None:
+                    decompress_all(None, p)
+                else:
+                    graphs["d", p].replay()
+                ring.signal_consumed(stream_d)
+            stream.wait_stream(stream_d)
+            return
         if mid is not None:
             mid[1].record(stream)
         if graphs is None:

@@ -221,6 +221,11 @@ int gp_ipc_open_event(const void* handle, void** event_out);
 int gp_event_destroy(void* event);
 int gp_event_record(void* event, void* stream);
 int gp_stream_wait_event(void* stream, void* event);
+/* As above, but inside a CUDA-graph capture they become external event record
+ * / wait nodes, so a replayed graph can signal, or wait for, another process's
+ * stream (per-frame hand-off of the peer transport). */
+int gp_event_record_external(void* event, void* stream);
+int gp_stream_wait_event_external(void* stream, void* event);
 /* Device-to-device (local or peer) async copy on `stream`. */
 int gp_copy_async(void* dst, const void* src, size_t bytes, void* stream);
 

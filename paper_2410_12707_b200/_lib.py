@@ -68,6 +68,8 @@ _SIGS = {
     "gp_event_destroy": (c_int, [c_void_p]),
     "gp_event_record": (c_int, [c_void_p, c_void_p]),
     "gp_stream_wait_event": (c_int, [c_void_p, c_void_p]),
+    "gp_event_record_external": (c_int, [c_void_p, c_void_p]),
+    "gp_stream_wait_event_external": (c_int, [c_void_p, c_void_p]),
     "gp_copy_async": (c_int, [c_void_p, c_void_p, c_size_t, c_void_p]),
 }
 IPC_HANDLE_BYTES = 64

@@ -424,6 +424,22 @@ int gp_event_record(void* event, void* stream) {
 int gp_stream_wait_event(void* stream, void* event) {
   return cuda_status(cudaStreamWaitEvent(as_stream(stream), static_cast<cudaEvent_t>(event), 0));
 }
+// the same inside a CUDA-graph capture as real (external) event record / wait
+// nodes: another process's stream or graph can then wait on a record made by
+// a graph replay here, and a graph can wait on another process's record
+static bool capturing(cudaStream_t s) {
+  cudaStreamCaptureStatus st = cudaStreamCaptureStatusNone;
+  return cudaStreamIsCapturing(s, &st) == cudaSuccess && st == cudaStreamCaptureStatusActive;
+}
+int gp_event_record_external(void* event, void* stream) {
+  const cudaStream_t s = as_stream(stream);
+  if (!capturing(s)) return cuda_status(cudaEventRecord(static_cast<cudaEvent_t>(event), s));
+  return cuda_status(cudaEventRecordWithFlags(static_cast<cudaEvent_t>(event), s, cudaEventRecordExternal));
+}
+int gp_stream_wait_event_external(void* stream, void* event) {
+  const cudaStream_t s = as_stream(stream);
+  return cuda_status(cudaStreamWaitEvent(s, static_cast<cudaEvent_t>(event), capturing(s) ? cudaEventWaitExternal : 0));
+}
 int gp_copy_async(void* dst, const void* src, size_t bytes, void* stream) {
   if ((!dst || !src) && bytes) return GP_ERR_INVALID_ARGUMENT;
   return cuda_status(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToDevice, as_stream(stream)));

@@ -106,8 +106,48 @@ class PeerRing:
         raise_for_status(self.L.gp_stream_wait_event(stream.cuda_stream, self.next_consumed),
                          "gp_stream_wait_event")
 
+    # ---- per-frame hand-off (optional): one interprocess event per frame and
+    # buffer parity, recorded after that frame's copy, so the successor can
+    # decompress each frame as soon as it lands instead of after the last one.
+    # Records and waits are "external", i.e. real event nodes inside captured
+    # CUDA graphs.
+    def enable_frame_events(self, nframes: int, cpu_group=None) -> None:
+        L = self.L
+        with torch.cuda.device(self.device):
+            self.frame_sent = [[ctypes.c_void_p() for _ in range(nframes)] for _ in range(2)]
+            handles = []
+            for par in range(2):
+                for i in range(nframes):
+                    h = (ctypes.c_char * _lib.IPC_HANDLE_BYTES)()
+                    raise_for_status(L.gp_ipc_event_create(ctypes.byref(self.frame_sent[par][i]), h),
+                                     "gp_ipc_event_create")
+                    handles.append(bytes(h))
+            objs = [None] * self.world
+            dist.all_gather_object(objs, handles, group=cpu_group)
+            prv = (self.rank - 1) % self.world
+            self.prev_frame_sent = [[ctypes.c_void_p() for _ in range(nframes)] for _ in range(2)]
+            for par in range(2):
+                for i in range(nframes):
+                    raise_for_status(L.gp_ipc_open_event(_handle(objs[prv][par * nframes + i]),
+                                                         ctypes.byref(self.prev_frame_sent[par][i])),
+                                     "gp_ipc_open_event")
+
+    def signal_frame_sent(self, parity: int, i: int, stream) -> None:
+        raise_for_status(self.L.gp_event_record_external(self.frame_sent[parity & 1][i], stream.cuda_stream),
+                         "gp_event_record_external")
+
+    def wait_frame_sent(self, parity: int, i: int, stream) -> None:
+        raise_for_status(self.L.gp_stream_wait_event_external(stream.cuda_stream,
+                                                              self.prev_frame_sent[parity & 1][i]),
+                         "gp_stream_wait_event_external")
+
     def close(self) -> None:
         L = self.L
+        for lst in getattr(self, "frame_sent", []):
+            for ev in lst:
+                if ev.value:
+                    L.gp_event_destroy(ev)
+        self.frame_sent = []
         if self.peer_base.value:
             L.gp_ipc_close_mem(self.peer_base)
             self.peer_base = ctypes.c_void_p()

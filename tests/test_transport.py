@@ -271,6 +271,128 @@ def test_peer_ring_world2(cuda, pull, shared):
     assert res == {0: True, 1: True}, res
 
 
+def _peer_frames_worker(rank, world, port, q, shared=False):
+    """The bench's N>1 step shape: several frames per step pushed into the
+    successor's buffer by the copy engines, each with its own interprocess
+    event recorded inside a captured CUDA graph, and the successor's
+    decompress graph -- on its own stream, overlapping the compress graph --
+    waiting per frame.  Fresh data every step, so a frame decompressed before
+    its copy landed (the same parity's frame of two steps earlier) is caught."""
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    try:
+        import paper_2410_12707_b200 as P
+        from paper_2410_12707_b200 import _lib
+        from paper_2410_12707_b200.peer import PeerRing
+
+        dev = torch.device("cuda", 0 if shared else rank)
+        torch.cuda.set_device(dev)
+        if shared:
+            dist.init_process_group("gloo", rank=rank, world_size=world)
+            cpu = None
+        else:
+            dist.init_process_group("nccl", rank=rank, world_size=world, device_id=dev)
+            cpu = dist.new_group(backend="gloo")
+        L = _lib.lib()
+        specs = [(200_003, 50.0), (350_011, 10.0), (120_007, 100.0)]
+        ks = [P.select_k(d, r) for d, r in specs]
+        fbs = [16 + 12 * k for k in ks]
+        offs = [sum((fb + 255) // 256 * 256 for fb in fbs[:i]) for i in range(len(fbs))]
+        ring = PeerRing(sum((fb + 255) // 256 * 256 for fb in fbs), dev, cpu)
+        ring.enable_frame_events(len(specs), cpu)
+        xs = [torch.empty(d, device=dev) for d, _ in specs]
+        frames = [torch.empty(fb, dtype=torch.uint8, device=dev) for fb in fbs]
+        outs = [torch.empty(d, device=dev) for d, _ in specs]
+        wsb = max(L.gp_topk_workspace_bytes(d, 0) for d, _ in specs)
+        ws = torch.zeros(wsb, dtype=torch.uint8, device=dev)
+        L.gp_workspace_init(ws.data_ptr(), wsb, torch.cuda.current_stream(dev).cuda_stream)
+        err = torch.zeros(1, dtype=torch.int32, device=dev)
+        st, cs, sd, side = (torch.cuda.Stream(dev) for _ in range(4))
+
+        def comp(par):
+            cur = torch.cuda.current_stream(dev)
+            cs.wait_stream(cur)
+            for i, (d, _) in enumerate(specs):
+                assert L.gp_topk_compress_frame(xs[i].data_ptr(), 0, d, ks[i], frames[i].data_ptr(), ws.data_ptr(),
+                                                wsb, cur.cuda_stream) == 0
+                done = torch.cuda.Event()
+                done.record(cur)
+                cs.wait_event(done)
+                ring.copy(ring.peer_recv(par) + offs[i], frames[i].data_ptr(), fbs[i], cs)
+                ring.signal_frame_sent(par, i, cs)
+            cur.wait_stream(cs)
+
+        def dec(par):
+            cur = torch.cuda.current_stream(dev)
+            for i, (d, _) in enumerate(specs[::-1]):  # not the send order
+                i = len(specs) - 1 - i
+                ring.wait_frame_sent(par, i, cur)
+                assert L.gp_topk_decompress_frame(ring.recv(par) + offs[i], ks[i], specs[i][0], outs[i].data_ptr(),
+                                                  0, 0, err.data_ptr(), cur.cuda_stream) == 0
+
+        graphs = {}
+        ok = True
+        prv = (rank - 1) % world
+        for step_no in range(8):
+            par = step_no & 1
+            st.wait_stream(sd)
+            ring.wait_consumed(st)
+            with torch.cuda.stream(st):
+                for i, (d, _) in enumerate(specs):
+                    xs[i].copy_(torch.randn(d, generator=torch.Generator().manual_seed(97 * step_no + 13 * i + rank)))
+                if step_no < 2:  # eager first (kernel attributes), then capture this parity's graphs
+                    comp(par)
+                else:
+                    graphs["c", par].replay()
+            dist.barrier(group=cpu)
+            with torch.cuda.stream(sd):
+                if step_no < 2:
+                    dec(par)
+                else:
+                    graphs["d", par].replay()
+                ring.signal_consumed(sd)
+            torch.cuda.synchronize(dev)
+            for i, (d, r) in enumerate(specs):
+                src = torch.randn(d, generator=torch.Generator().manual_seed(97 * step_no + 13 * i + prv)).numpy()
+                vals, idx, _ = O.topk_compress(src, r)
+                ok &= np.array_equal(outs[i].cpu().numpy().view(np.uint32), O.topk_decompress(vals, idx, d).view(np.uint32))
+            ok &= int(err.item()) == 0
+            if step_no < 2:
+                side.wait_stream(st)
+                for name, fn in (("c", comp), ("d", dec)):
+                    g = torch.cuda.CUDAGraph()
+                    with torch.cuda.graph(g, stream=side):
+                        fn(par)
+                    graphs[name, par] = g
+                torch.cuda.synchronize(dev)
+                dist.barrier(group=cpu)
+        dist.barrier()
+        ring.close()
+        dist.destroy_process_group()
+        q.put((rank, bool(ok)))
+    except Exception as e:
+        q.put((rank, repr(e)))
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("shared", [False, True], ids=["2gpu", "1gpu"])
+def test_peer_ring_frame_events_in_graphs(cuda, shared):
+    """Per-frame interprocess events recorded and waited on inside captured
+    CUDA graphs, decompress overlapping the compress phase: every frame of
+    every step equals the oracle's (bench.py's N>1 step, GP_BENCH_FRAME_HANDOFF)."""
+    if not shared and torch.cuda.device_count() < 2:
+        pytest.skip("needs 2 GPUs (run under gpurun --gpus 2)")
+    ctx = tmp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    ps = [ctx.Process(target=_peer_frames_worker, args=(r, 2, port, q, shared)) for r in range(2)]
+    for p in ps:
+        p.start()
+    res = dict(q.get(timeout=300) for _ in range(2))
+    for p in ps:
+        p.join(timeout=60)
+    assert res == {0: True, 1: True}, res
+
+
 def test_opdata_envelope_cpu():
     """The OpData envelope (opdag.py:67-86) ahead of every pipeline message:
     iteration, micro-batch, link, kind, compress_cfg and shape; a receiver
