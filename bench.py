@@ -685,7 +685,10 @@ def run_ours(args, rank, world, local_rank):
                                       "by the successor's decompress kernels reading this rank's frames over "
                                       "NVLink (CUDA IPC peer memory, no copy; interprocess-event handoff)" if pull else
                                       "by copy engines into the successor's buffer over NVLink (CUDA IPC, "
-                                      "overlapping the next compress; interprocess-event handoff)" if peer else
+                                      "overlapping the next compress; "
+                                      + ("one interprocess event per frame, each unit decompressed as soon as its "
+                                         "frame lands)" if frame_handoff else "interprocess-event handoff)")
+                                      if peer else
                                       "over NCCL P2P (batch_isend_irecv)"))},
         "roofline": {"bound": "hbm", "kernel": "compress_kernel<f32> (cooperative, 1 CTA/SM)",
                      "achieved": round(achieved, 1), "peak": peak, "peak_kind": peak_kind, "unit": "GB/s",
