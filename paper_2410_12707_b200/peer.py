@@ -143,18 +143,18 @@ class PeerRing:
 
     def close(self) -> None:
         L = self.L
-        for lst in getattr(self, "frame_sent", []):
+        for lst in getattr(self, "frame_sent", []) + getattr(self, "prev_frame_sent", []):
             for ev in lst:
                 if ev.value:
                     L.gp_event_destroy(ev)
-        self.frame_sent = []
+        self.frame_sent, self.prev_frame_sent = [], []
         if self.peer_base.value:
             L.gp_ipc_close_mem(self.peer_base)
             self.peer_base = ctypes.c_void_p()
-        for ev in (self.sent, self.consumed):
+        for ev in (self.sent, self.consumed, self.prev_sent, self.next_consumed):
             if ev.value:
                 L.gp_event_destroy(ev)
-        self.sent = self.consumed = ctypes.c_void_p()
+        self.sent = self.consumed = self.prev_sent = self.next_consumed = ctypes.c_void_p()
         if self.recv_base.value:
             L.gp_peer_free(self.recv_base)
             self.recv_base = ctypes.c_void_p()
