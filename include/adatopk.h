@@ -88,6 +88,17 @@ int gp_topk_compress(const void* x, int dtype, int64_t d, int64_t k,
 int gp_topk_compress_frame(const void* x, int dtype, int64_t d, int64_t k,
                            void* frame_out, void* ws, size_t ws_bytes, void* stream);
 
+/* Short vectors can be compressed by a single thread-block cluster -- one HBM
+ * read into the CTAs' shared memory, DSMEM histograms, cluster barriers --
+ * instead of the cooperative grid (identical results).  mode 1 (default): the
+ * cluster kernel for vectors of at most 49,152 elements, where it is the
+ * faster one on B200 (~2x at 16K elements); 2: for every vector that fits one
+ * 8-CTA cluster (up to 425,984 fp32 / 851,968 bf16 / 212,992 fp64 elements,
+ * within max_ctas);
+ * 0: never (also when the environment sets GP_NO_CLUSTER=1).  Returns the
+ * previous mode.  Process-wide; for A/B measurements and tests. */
+int gp_set_cluster_path(int mode);
+
 /* decompress `mode` bits */
 #define GP_DECOMPRESS_RESIDUAL 1   /* add into `out` instead of zero-filling (extension) */
 #define GP_DECOMPRESS_TRUSTED  2   /* indices written by gp_topk_compress* and unmodified: strictly

@@ -27,6 +27,7 @@ FRAME_HEADER_BYTES = 16
 _SIGS = {
     "gp_version": (ctypes.c_char_p, []),
     "gp_select_k": (c_int, [c_int64, c_double, POINTER(c_int64)]),
+    "gp_set_cluster_path": (c_int, [c_int]),
     "gp_wire_bytes": (c_int, [c_int64, c_double, POINTER(c_int64)]),
     "gp_topk_workspace_bytes": (c_size_t, [c_int64, c_int]),
     "gp_workspace_init": (c_int, [c_void_p, c_size_t, c_void_p]),

@@ -25,7 +25,7 @@ COMMON = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O2", "--expt-r
 # fmad is irrelevant to the integer select path; the Eq. 6 bookkeeping has only
 # mul/div, but keep contraction off there so the IEEE order is explicit.
 PER_FILE = {"gp_capi.cu": ["--fmad=false"]}
-SOURCES = ["gp_compress.cu", "gp_decompress.cu", "gp_capi.cu"]
+SOURCES = ["gp_compress.cu", "gp_cluster.cu", "gp_decompress.cu", "gp_capi.cu"]
 
 
 def nvcc() -> str:

@@ -96,6 +96,8 @@ extern "C" {
 
 const char* gp_version(void) { return "adatopk-b200 0.1.0 sm_100a"; }
 
+int gp_set_cluster_path(int mode) { return gp::set_cluster_path(mode); }
+
 // Development aid (not part of the public header): when non-NULL, every
 // compress launch writes per-CTA stage timestamps (globaltimer ns, clock64)
 // into this device buffer of G*32 u64.

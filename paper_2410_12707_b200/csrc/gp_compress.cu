@@ -1600,6 +1600,11 @@ static int launch_compress_t(CompressArgs a, const DeviceInfo& dev, cudaStream_t
 }
 
 int launch_compress(int dtype, CompressArgs a, const DeviceInfo& dev, cudaStream_t stream) {
+  // vectors that fit one cluster's shared memory: gp_cluster.cu (no grid barriers)
+  if (!(a.k == a.d && a.k_dev == nullptr)) {
+    const int rc = launch_compress_cluster(dtype, a, dev, stream);
+    if (rc >= 0) return rc;
+  }
   switch (dtype) {
     case 0: return launch_compress_t<TraitsF32>(a, dev, stream);
     case 1: return launch_compress_t<TraitsBF16>(a, dev, stream);

@@ -80,6 +80,10 @@ struct DeviceInfo {
 };
 
 int launch_compress(int dtype, CompressArgs a, const DeviceInfo& dev, cudaStream_t stream);
+// one-cluster compress of a short vector (gp_cluster.cu); -1 when not applicable
+int launch_compress_cluster(int dtype, const CompressArgs& a, const DeviceInfo& dev, cudaStream_t stream);
+int cluster_path_mode();
+int set_cluster_path(int mode);  // returns the previous mode
 size_t compress_workspace_layout(uint64_t d, int dtype, size_t ws_bytes, WsLayout* out);
 size_t compress_workspace_bytes(uint64_t d, int dtype);
 size_t workspace_state_bytes(size_t ws_bytes);
