@@ -89,6 +89,22 @@ def main():
     fa, _ = compress_frame(x[:1000].contiguous(), 1.0)
     check_frame("keep-all", x[:1000].cpu().numpy(), 1.0, fa)
 
+    # the single-cluster kernel (gp_cluster.cu): default-routed short vectors,
+    # and every vector that fits one cluster (mode 2), incl. ties, unaligned, bf16, fp64
+    for name, t, r, dt in (("cluster f32 (default route)", x[:40_000].contiguous(), 10.0, 0),
+                           ("cluster f32 tail", x[:33].contiguous(), 3.0, 0)):
+        fr, _ = compress_frame(t, r, dtype=dt)
+        check_frame(name, t.cpu().numpy(), r, fr)
+    prev = L.gp_set_cluster_path(2)
+    for name, t, r, dt in (("cluster f32", x[:n].contiguous() if n <= 425_984 else x[:400_000].contiguous(), 100.0, 0),
+                           ("cluster ties", ties[:200_000].contiguous(), 3.0, 0),
+                           ("cluster unaligned", x[5:5 + 100_000], 10.0, 0),
+                           ("cluster bf16", xb[:300_000].contiguous(), 10.0, 1),
+                           ("cluster f64", x.double()[:200_000].contiguous(), 100.0, 2)):
+        fr, _ = compress_frame(t, r, dtype=dt)
+        check_frame(name, (t.float() if dt == 1 else t).cpu().numpy(), r, fr)
+    L.gp_set_cluster_path(prev)
+
     # four concurrent capped grids, a workspace per stream
     sts = [torch.cuda.Stream(DEV) for _ in range(4)]
     xs = [torch.randn(n, device=DEV, generator=g) for _ in range(4)]
