@@ -91,9 +91,9 @@ int gp_topk_compress_frame(const void* x, int dtype, int64_t d, int64_t k,
 /* Short vectors can be compressed by a single thread-block cluster -- one HBM
  * read into the CTAs' shared memory, DSMEM histograms, cluster barriers --
  * instead of the cooperative grid (identical results).  mode 1 (default): the
- * cluster kernel for vectors of at most 49,152 elements, where it is the
- * faster one on B200 (~2x at 16K elements); 2: for every vector that fits one
- * 8-CTA cluster (up to 425,984 fp32 / 851,968 bf16 / 212,992 fp64 elements,
+ * cluster kernel for vectors of at most 98,304 elements, where it is the
+ * faster one on B200 (1.4-1.7x cold at 1K-64K elements); 2: for every vector that fits one
+ * 8-CTA cluster (up to 393,216 fp32 / 786,432 bf16 / 196,608 fp64 elements,
  * within max_ctas);
  * 0: never (also when the environment sets GP_NO_CLUSTER=1).  Returns the
  * previous mode.  Process-wide; for A/B measurements and tests. */

@@ -5,14 +5,14 @@
 // 79-94, `np.argsort(-np.abs(flat), kind="stable")[:k]`, kept indices in
 // ascending order; the integer key of gp_common.cuh, ties to the lower index),
 // for vectors that fit in the shared memory of one cluster (up to 8 CTAs x
-// 208 KiB: 425,984 fp32 / 851,968 bf16 / 212,992 fp64 elements).
+// 192 KiB: 393,216 fp32 / 786,432 bf16 / 196,608 fp64 elements).
 //
 // The cooperative kernel's latency floor on short vectors is its chain of grid
 // barriers through L2 (~20 us cold whatever the length or ratio).  On B200
 // (scripts/cluster_probe.py, each launch after an L2 flush) this kernel takes
-// 10-12 us for up to 16K fp32 elements and 18 us at 64K, against 20-24 us;
-// warm, the cooperative grid is ahead from ~48K elements on, so the default
-// routing sends vectors of up to 49,152 elements here.  A 16-CTA
+// 12-15 us for up to 64K fp32 elements and 16-20 us at 128K, against 20-24 us;
+// warm, the cooperative grid is level from ~128K elements on, so the default
+// routing sends vectors of up to 98,304 elements here.  A 16-CTA
 // (non-portable) cluster costs ~10 us more than an 8-CTA one, so clusters are
 // capped at 8 CTAs (GP_CL_MAX_CTAS).  Here the
 // vector is read from HBM exactly once into the CTAs' shared memory and every
@@ -23,11 +23,16 @@
 //   select    radix select of the k-th largest key, 11-bit digits from the top
 //             (3 passes for 32-bit keys, 6 for fp64): every CTA histograms the
 //             digit of its keys still matching the prefix, one cluster
-//             barrier, then every CTA sums the digit's bins over all CTAs
-//             (DSMEM loads, no second barrier) and finds the crossing itself
-//             -> threshold key T and the tie quota q (T-keys to keep)
-//   count     per warp segment: keys > T and keys == T; CTA totals published,
-//             one cluster barrier, each CTA sums the earlier CTAs' totals
+//             barrier, then one warp per CTA finds the crossing over the
+//             cluster (DSMEM loads: 32-bin group sums, then the bins of one
+//             group; every CTA computes the same result, no second barrier)
+//             -> threshold key T and the tie quota q (T-keys to keep).  Pass 1
+//             also lists the keys of pass 0's bin (16 KiB of smem) and counts
+//             per warp the keys above it, so the later passes read the list
+//             (a CTA whose list overflows scans its slice instead)
+//   count     per warp segment: keys > T and keys == T (from the list when it
+//             is complete); CTA totals published, one cluster barrier, each
+//             CTA sums the earlier CTAs' totals
 //   write     output position of a kept element = (#keys > T before it) +
 //             min(q, #keys == T before it): one packed warp scan per step
 //
@@ -44,9 +49,10 @@ namespace cg = cooperative_groups;
 constexpr int kClThreads = 1024;
 constexpr int kClDigitBits = 11;
 constexpr int kClBins = 1 << kClDigitBits;
-constexpr uint32_t kClDataBytes = 208u * 1024u;  // the resident slice of the vector
-constexpr uint32_t kClSmallBytes = (2u * kClBins + 64u + 16u + 64u + 4u) * 4u;
-constexpr uint32_t kClSmemBytes = kClDataBytes + kClSmallBytes;
+constexpr uint32_t kClDataBytes = 192u * 1024u;  // the resident slice of the vector
+constexpr uint32_t kClListBytes = 16u * 1024u;   // pass-1 list: (slice index, bits) of the keys in the top bin
+constexpr uint32_t kClSmallBytes = (2u * kClBins + 64u + 16u + 64u + 4u + 32u + 128u) * 4u;
+constexpr uint32_t kClSmemBytes = kClDataBytes + kClListBytes + kClSmallBytes;
 constexpr int kClMaxCtas = 16;  // DSMEM reduction width (a 16-CTA cluster only with GP_CL_MAX_CTAS=16)
 #ifndef GP_CL_MAX_CTAS
 #define GP_CL_MAX_CTAS 8
@@ -56,7 +62,7 @@ constexpr int kClMaxCtas = 16;  // DSMEM reduction width (a 16-CTA cluster only 
 #endif
 constexpr uint32_t kClMinPerCta = GP_CL_MIN_PER_CTA;  // elements per CTA below which the cluster shrinks
 #ifndef GP_CL_AUTO_MAX
-#define GP_CL_AUTO_MAX 49152
+#define GP_CL_AUTO_MAX 98304
 #endif
 constexpr uint32_t kClAutoMax = GP_CL_AUTO_MAX;  // default routing: vectors up to this many elements
 
@@ -67,18 +73,6 @@ __device__ __forceinline__ void cluster_arrive_release() {
 }
 __device__ __forceinline__ void cluster_wait_acquire() {
   asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
-}
-
-// 1024-thread exclusive scan, two barriers; sh32 holds 64 words.
-__device__ __forceinline__ uint32_t cl_block_excl_scan(uint32_t v, uint32_t* sh32, uint32_t* total) {
-  const uint32_t lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  const uint32_t x = warp_incl_scan(v);
-  if (lane == 31) sh32[w] = x;
-  __syncthreads();
-  if (w == 0) sh32[32 + lane] = warp_incl_scan(sh32[lane]);
-  __syncthreads();
-  *total = sh32[63];
-  return (w ? sh32[32 + w - 1] : 0u) + x - v;
 }
 
 template <class Tr>
@@ -122,12 +116,17 @@ __global__ void __launch_bounds__(kClThreads, 1) compress_cluster_kernel(const C
   constexpr int KB = Tr::kKeyBits;              // keys are < 2^KB
   constexpr int NP = (KB + kClDigitBits - 1) / kClDigitBits;
 
+  constexpr uint32_t kListCap = kClListBytes / (4u + (uint32_t)sizeof(Bits));
+
   extern __shared__ __align__(16) unsigned char smem[];
-  uint32_t* hbuf = reinterpret_cast<uint32_t*>(smem + kClDataBytes);  // 2 x kClBins (pass parity)
-  uint32_t* sh32 = hbuf + 2 * kClBins;                                // 64
-  uint32_t* res = sh32 + 64;                                          // 16
+  Bits* lbits = reinterpret_cast<Bits*>(smem + kClDataBytes);              // list: bits, then slice indices
+  uint32_t* lidx = reinterpret_cast<uint32_t*>(smem + kClDataBytes + kListCap * sizeof(Bits));
+  uint32_t* hbuf = reinterpret_cast<uint32_t*>(smem + kClDataBytes + kClListBytes);  // 2 x kClBins (pass parity)
+  uint32_t* res = hbuf + 2 * kClBins + 64;                            // 16 (res[8]: list length)
   uint32_t* wcnt = res + 16;                                          // per-warp (>T, ==T) counts
   uint32_t* ccnt = wcnt + 64;                                         // this CTA's totals (read remotely)
+  uint32_t* wabv = ccnt + 4;                                          // per warp: keys above pass 1's bin
+  uint32_t* gbuf = wabv + 32;                                         // 2 x 64 group sums (pass parity)
   const uint32_t xs = smem_addr(smem);
 
   cg::cluster_group cl = cg::this_cluster();
@@ -172,6 +171,7 @@ __global__ void __launch_bounds__(kClThreads, 1) compress_cluster_kernel(const C
   Elem* xe = reinterpret_cast<Elem*>(smem);
   for (uint32_t i = first_scalar + tid; i < n; i += kClThreads) xe[i] = src[i];
   for (uint32_t i = tid; i < 2u * kClBins; i += kClThreads) hbuf[i] = 0u;
+  if (tid == 0) res[8] = 0u;
   cp_async_wait<0>();
   __syncthreads();
   CL_STAMP(1);
@@ -179,6 +179,10 @@ __global__ void __launch_bounds__(kClThreads, 1) compress_cluster_kernel(const C
   const uint32_t nfull = n / EPS;                // complete 16-byte vectors
   const uint32_t nv = (n + EPS - 1) / EPS;       // vectors, the last one possibly partial
   const uint32_t nlast = n - (nv ? nv - 1 : 0u) * EPS;
+  // warp segments (contiguous vectors, index order) of pass 1, the count and the write
+  const uint32_t S = (nv + 31u) / 32u;
+  const uint32_t v0 = min(nv, w * S), v1 = min(nv, v0 + S);
+  bool list_ok = false;  // pass 1's list holds every key of its bin (this CTA)
 
   // ---- radix select: T = the k-th largest key over the cluster, q = T-keys to keep
   Key P = 0;
@@ -198,40 +202,108 @@ __global__ void __launch_bounds__(kClThreads, 1) compress_cluster_kernel(const C
       const Key kk = Tr::key(b);
       if ((kk >> hi) == P) atomicAdd(&h[(uint32_t)(kk >> lo) & mask], 1u);
     };
-    for (uint32_t v = tid; v < nfull; v += kClThreads) {
-      const uint4 q4 = ld_shared_v4(xs + v * 16u);
+    if (p == 1) {
+      // pass 1, over the warp segments: the keys of pass 0's bin are also
+      // listed (their number is small unless the bin is crowded), and each
+      // warp counts its keys above the bin (all > T); later passes and the
+      // count then read the list instead of the slice
+      uint32_t abv = 0;
+      for (uint32_t v = v0 + lane; v < v1; v += 32u) {
+        const uint4 q4 = ld_shared_v4(xs + v * 16u);
+        const uint32_t ne = v + 1u == nv ? nlast : (uint32_t)EPS;
 #pragma unroll
-      for (int e = 0; e < EPS; ++e) add(Tr::lane(q4, e));
+        for (int e = 0; e < EPS; ++e) {
+          const Bits b = Tr::lane(q4, e);
+          const Key kk = Tr::key(b);
+          if ((uint32_t)e < ne) {
+            const Key top = kk >> hi;
+            if (top == P) {  // rare: one list slot per key (a per-warp reservation measured 2x slower)
+              atomicAdd(&h[(uint32_t)(kk >> lo) & mask], 1u);
+              const uint32_t j = atomicAdd(&res[8], 1u);
+              if (j < kListCap) {
+                lbits[j] = b;
+                lidx[j] = v * (uint32_t)EPS + (uint32_t)e;
+              }
+            } else if (top > P) {
+              ++abv;
+            }
+          }
+        }
+      }
+      abv = warp_sum(abv);
+      if (lane == 0) wabv[w] = abv;
+    } else if (p >= 2 && list_ok) {
+      const uint32_t nl = res[8];
+      for (uint32_t j = tid; j < nl; j += kClThreads) add(lbits[j]);
+    } else {
+      for (uint32_t v = tid; v < nfull; v += kClThreads) {
+        const uint4 q4 = ld_shared_v4(xs + v * 16u);
+#pragma unroll
+        for (int e = 0; e < EPS; ++e) add(Tr::lane(q4, e));
+      }
+      if (tid < n - nfull * EPS) add(cl_elem_bits<Tr>(xe, nfull * EPS + tid));
     }
-    if (tid < n - nfull * EPS) add(cl_elem_bits<Tr>(xe, nfull * EPS + tid));
+    // group sums (32 bins each) for the two-level cluster reduction below
+    const uint32_t NB = 1u << width, NG = NB / 32u;  // NB >= 256: 8..64 groups
+    uint32_t* gs = gbuf + (p & 1) * 64u;
+    __syncthreads();
+    for (uint32_t g = w; g < NG; g += 32u) {
+      const uint32_t t = warp_sum(h[g * 32u + lane]);
+      if (lane == 0) gs[g] = t;
+    }
     CL_STAMP(2 + 3 * p);
     cl.sync();
     CL_STAMP(3 + 3 * p);
-    // every CTA sums the bins over the cluster; thread t owns descending bins
-    // NB-1-2t and NB-2-2t (one 8-byte DSMEM load per CTA)
-    const uint32_t NB = 1u << width;
-    uint32_t h0 = 0, h1 = 0;  // bins b0 = NB-1-2t (higher), b1 = b0-1
-    if (2u * tid < NB) {  // all loads issued before the first is consumed
-      const uint32_t b1 = NB - 2u - 2u * tid;
-      uint2 v[kClMaxCtas];
+    if (p == 1) list_ok = res[8] <= kListCap;  // final: the cluster barrier ordered every append
+    // warp 0 finds the crossing: the group over the cluster's group sums (DSMEM,
+    // lane l owns groups NG-1-2l, NG-2-2l), then the bin inside that group (lane l
+    // owns bin 31-l of it); every CTA computes the same result, no second barrier
+    if (w == 0) {
+      uint32_t g0 = 0, g1 = 0;  // groups a = NG-1-2l (higher), b = a-1
+      const bool own = 2u * lane < NG;
+      if (own) {
+        uint2 v[kClMaxCtas];
+        const uint32_t gb = NG - 2u - 2u * lane;
 #pragma unroll
-      for (int r = 0; r < kClMaxCtas; ++r)
-        v[r] = (uint32_t)r < nc ? *reinterpret_cast<const uint2*>(cl.map_shared_rank(h + b1, r)) : make_uint2(0u, 0u);
+        for (int r = 0; r < kClMaxCtas; ++r)
+          v[r] = (uint32_t)r < nc ? *reinterpret_cast<const uint2*>(cl.map_shared_rank(gs + gb, r)) : make_uint2(0u, 0u);
 #pragma unroll
-      for (int r = 0; r < kClMaxCtas; ++r) {
-        h1 += v[r].x;
-        h0 += v[r].y;
+        for (int r = 0; r < kClMaxCtas; ++r) {
+          g1 += v[r].x;
+          g0 += v[r].y;
+        }
       }
-    }
-    uint32_t tot;
-    const uint32_t above = cl_block_excl_scan(h0 + h1, sh32, &tot);
-    if (2u * tid < NB) {
-      if (above < kr && kr <= above + h0) {
-        res[0] = NB - 1u - 2u * tid;
-        res[1] = above;
-      } else if (above + h0 < kr && kr <= above + h0 + h1) {
-        res[0] = NB - 2u - 2u * tid;
-        res[1] = above + h0;
+      const uint32_t incl = warp_incl_scan(g0 + g1);
+      const uint32_t ex = incl - (g0 + g1);
+      uint32_t hit = 0, gabove = 0, grp = 0;
+      if (own) {
+        if (ex < kr && kr <= ex + g0) {
+          hit = 1u;
+          grp = NG - 1u - 2u * lane;
+          gabove = ex;
+        } else if (ex + g0 < kr && kr <= ex + g0 + g1) {
+          hit = 1u;
+          grp = NG - 2u - 2u * lane;
+          gabove = ex + g0;
+        }
+      }
+      const uint32_t hb = __ballot_sync(kFull, hit != 0u);
+      GP_CHECK(__popc(hb) == 1);
+      const int src = __ffs(hb) - 1;
+      grp = __shfl_sync(kFull, grp, src);
+      gabove = __shfl_sync(kFull, gabove, src);
+      const uint32_t bin = grp * 32u + 31u - lane;
+      uint32_t hv[kClMaxCtas];
+#pragma unroll
+      for (int r = 0; r < kClMaxCtas; ++r) hv[r] = (uint32_t)r < nc ? *cl.map_shared_rank(h + bin, r) : 0u;
+      uint32_t hs = 0;
+#pragma unroll
+      for (int r = 0; r < kClMaxCtas; ++r) hs += hv[r];
+      const uint32_t bi = warp_incl_scan(hs);
+      const uint32_t bex = gabove + bi - hs;
+      if (bex < kr && kr <= bex + hs) {
+        res[0] = bin;
+        res[1] = bex;
       }
     }
     __syncthreads();
@@ -244,9 +316,33 @@ __global__ void __launch_bounds__(kClThreads, 1) compress_cluster_kernel(const C
   const uint32_t q = kr;  // keys equal to T that are kept: the q lowest-indexed ones
 
   // ---- count: per warp segment (contiguous vectors, index order) keys > T and == T
-  const uint32_t S = (nv + 31u) / 32u;
-  const uint32_t v0 = min(nv, w * S), v1 = min(nv, v0 + S);
-  {
+  if (list_ok) {
+    // keys > T: those above pass 1's bin (counted there) and the listed ones
+    // above T; keys == T are all listed
+    if (tid < 32) {
+      wcnt[tid] = wabv[tid];
+      wcnt[32 + tid] = 0u;
+    }
+    __syncthreads();
+    const uint32_t nl = res[8];
+    for (uint32_t j = tid; j < nl; j += kClThreads) {
+      const Key kk = Tr::key(lbits[j]);
+      const uint32_t ws = (lidx[j] / (uint32_t)EPS) / S;  // the warp segment holding the entry
+      if (kk > T) atomicAdd(&wcnt[ws], 1u);
+      else if (kk == T) atomicAdd(&wcnt[32 + ws], 1u);
+    }
+    __syncthreads();
+    if (w == 0) {
+      const uint32_t g = wcnt[lane], e = wcnt[32 + lane];
+      const uint32_t gi = warp_incl_scan(g), ei = warp_incl_scan(e);
+      wcnt[lane] = gi - g;
+      wcnt[32 + lane] = ei - e;
+      if (lane == 31) {
+        ccnt[0] = gi;
+        ccnt[1] = ei;
+      }
+    }
+  } else {
     uint32_t gt = 0, eq = 0;
     for (uint32_t v = v0 + lane; v < v1; v += 32u) {
       const uint4 q4 = ld_shared_v4(xs + v * 16u);
@@ -297,6 +393,7 @@ __global__ void __launch_bounds__(kClThreads, 1) compress_cluster_kernel(const C
   }
   cluster_arrive_release();  // this CTA's remote reads are done; it waits before exiting
   __syncthreads();
+  CL_STAMP(23);
 
   // ---- write: kept (index, value) pairs in index order
   uint32_t gtb = res[4] + wcnt[w], eqb = res[5] + wcnt[32 + w];
@@ -316,6 +413,7 @@ __global__ void __launch_bounds__(kClThreads, 1) compress_cluster_kernel(const C
         }
       }
     }
+    if (!__any_sync(kFull, (gm | em) != 0u)) continue;  // nothing kept or tied in this step
     const uint32_t packed = (uint32_t)__popc(gm) | ((uint32_t)__popc(em) << 16);
     const uint32_t incl = warp_incl_scan(packed);
     const uint32_t tot = __shfl_sync(kFull, incl, 31);
@@ -442,8 +540,8 @@ int launch_compress_cluster(int dtype, const CompressArgs& a, const DeviceInfo& 
   const int mode = cluster_path_mode();
   if (mode == 0) return -1;
   // auto: only where it beats the cooperative grid (B200 A/B, scripts/cluster_probe.py:
-  // 16K fp32 elements 11-12 us vs 23-24 us cold, 32K 14-15 vs 23-24; at 64K 18 vs
-  // 21-22 cold but 17 vs 16 warm)
+  // 16K fp32 elements 14 us vs 22-24 us cold, 64K 14-15 vs 21-22 cold and 13-14 vs
+  // 15-16 warm; at 128K 16-20 vs 20-22 cold but 15-18 vs 15-17 warm)
   static const uint32_t auto_max = env_u32("GP_CL_AUTO_MAX", kClAutoMax);
   if (mode == 1 && a.d > auto_max) return -1;
   switch (dtype) {

@@ -24,8 +24,8 @@ from paper_2410_12707_b200 import _lib  # noqa: E402
 from scripts.graph_timing import graph_time  # noqa: E402
 
 CASES = [  # (dtype, d)
-    ("fp32", 16_384), ("fp32", 65_536), ("fp32", 262_144), ("fp32", 786_432), ("fp32", 851_968),
-    ("bf16", 524_288), ("bf16", 1_572_864), ("fp64", 131_072),
+    ("fp32", 65_536), ("fp32", 131_072), ("fp32", 196_608), ("fp32", 262_144), ("fp32", 393_216),
+    ("bf16", 262_144), ("bf16", 524_288), ("bf16", 786_432), ("fp64", 65_536), ("fp64", 131_072),
 ]
 SMALL = [("fp32", 1024), ("fp32", 4096), ("fp32", 8192), ("fp32", 16_384), ("fp32", 32_768), ("fp32", 65_536),
          ("bf16", 16_384), ("bf16", 65_536), ("fp64", 8192), ("fp64", 32_768)]

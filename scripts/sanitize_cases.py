@@ -91,12 +91,12 @@ def main():
 
     # the single-cluster kernel (gp_cluster.cu): default-routed short vectors,
     # and every vector that fits one cluster (mode 2), incl. ties, unaligned, bf16, fp64
-    for name, t, r, dt in (("cluster f32 (default route)", x[:40_000].contiguous(), 10.0, 0),
+    for name, t, r, dt in (("cluster f32 (default route)", x[:90_000].contiguous(), 10.0, 0),
                            ("cluster f32 tail", x[:33].contiguous(), 3.0, 0)):
         fr, _ = compress_frame(t, r, dtype=dt)
         check_frame(name, t.cpu().numpy(), r, fr)
     prev = L.gp_set_cluster_path(2)
-    for name, t, r, dt in (("cluster f32", x[:n].contiguous() if n <= 425_984 else x[:400_000].contiguous(), 100.0, 0),
+    for name, t, r, dt in (("cluster f32", x[:n].contiguous() if n <= 393_216 else x[:380_000].contiguous(), 100.0, 0),
                            ("cluster ties", ties[:200_000].contiguous(), 3.0, 0),
                            ("cluster unaligned", x[5:5 + 100_000], 10.0, 0),
                            ("cluster bf16", xb[:300_000].contiguous(), 10.0, 1),
