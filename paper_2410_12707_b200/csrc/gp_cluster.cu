@@ -395,12 +395,13 @@ __global__ void __launch_bounds__(kClThreads, 1) compress_cluster_kernel(const C
   __syncthreads();
   CL_STAMP(23);
 
-  // ---- write: kept (index, value) pairs in index order
+  // ---- write: kept (index, value) pairs in index order; two 32-vector steps
+  // per iteration, so their load -> scan -> store chains overlap
   uint32_t gtb = res[4] + wcnt[w], eqb = res[5] + wcnt[32 + w];
-  for (uint32_t vb = v0; vb < v1; vb += 32u) {
-    const uint32_t v = vb + lane;
-    uint32_t gm = 0, em = 0;
-    uint4 q4 = make_uint4(0u, 0u, 0u, 0u);
+  auto masks = [&](uint32_t v, uint4& q4, uint32_t& gm, uint32_t& em) {
+    gm = 0u;
+    em = 0u;
+    q4 = make_uint4(0u, 0u, 0u, 0u);
     if (v < v1) {
       q4 = ld_shared_v4(xs + v * 16u);
       const uint32_t ne = v + 1u == nv ? nlast : (uint32_t)EPS;
@@ -413,32 +414,42 @@ __global__ void __launch_bounds__(kClThreads, 1) compress_cluster_kernel(const C
         }
       }
     }
-    if (!__any_sync(kFull, (gm | em) != 0u)) continue;  // nothing kept or tied in this step
-    const uint32_t packed = (uint32_t)__popc(gm) | ((uint32_t)__popc(em) << 16);
-    const uint32_t incl = warp_incl_scan(packed);
-    const uint32_t tot = __shfl_sync(kFull, incl, 31);
-    if (gm | em) {
-      const uint32_t ex = incl - packed;
-      uint32_t g = gtb + (ex & 0xFFFFu), e2 = eqb + (ex >> 16);
-      const uint32_t base = i0 + v * (uint32_t)EPS;
+  };
+  auto emit = [&](uint32_t v, const uint4& q4, uint32_t gm, uint32_t em, uint32_t g, uint32_t e2) {
+    const uint32_t base = i0 + v * (uint32_t)EPS;
 #pragma unroll
-      for (int e = 0; e < EPS; ++e) {
-        if ((gm >> e) & 1u) {
-          const uint32_t pos = g + min(q, e2);
-          GP_CHECK(pos < k);
-          cl_write_out<Tr>(a, val_out, pos, base + e, Tr::lane(q4, e));
-          ++g;
-        } else if ((em >> e) & 1u) {
-          if (e2 < q) {
-            GP_CHECK(g + e2 < k);
-            cl_write_out<Tr>(a, val_out, g + e2, base + e, Tr::lane(q4, e));
-          }
-          ++e2;
+    for (int e = 0; e < EPS; ++e) {
+      if ((gm >> e) & 1u) {
+        const uint32_t pos = g + min(q, e2);
+        GP_CHECK(pos < k);
+        cl_write_out<Tr>(a, val_out, pos, base + e, Tr::lane(q4, e));
+        ++g;
+      } else if ((em >> e) & 1u) {
+        if (e2 < q) {
+          GP_CHECK(g + e2 < k);
+          cl_write_out<Tr>(a, val_out, g + e2, base + e, Tr::lane(q4, e));
         }
+        ++e2;
       }
     }
-    gtb += tot & 0xFFFFu;
-    eqb += tot >> 16;
+  };
+  for (uint32_t vb = v0; vb < v1; vb += 64u) {
+    const uint32_t va = vb + lane, vc = vb + 32u + lane;
+    uint4 qa, qc;
+    uint32_t ga, ea, gc, ec;
+    masks(va, qa, ga, ea);
+    masks(vc, qc, gc, ec);
+    if (!__any_sync(kFull, (ga | ea | gc | ec) != 0u)) continue;  // nothing kept or tied in either step
+    const uint32_t pa = (uint32_t)__popc(ga) | ((uint32_t)__popc(ea) << 16);
+    const uint32_t pc = (uint32_t)__popc(gc) | ((uint32_t)__popc(ec) << 16);
+    const uint32_t ia = warp_incl_scan(pa), ic = warp_incl_scan(pc);
+    const uint32_t ta = __shfl_sync(kFull, ia, 31), tc = __shfl_sync(kFull, ic, 31);
+    if (ga | ea) emit(va, qa, ga, ea, gtb + ((ia - pa) & 0xFFFFu), eqb + ((ia - pa) >> 16));
+    gtb += ta & 0xFFFFu;
+    eqb += ta >> 16;
+    if (gc | ec) emit(vc, qc, gc, ec, gtb + ((ic - pc) & 0xFFFFu), eqb + ((ic - pc) >> 16));
+    gtb += tc & 0xFFFFu;
+    eqb += tc >> 16;
   }
   CL_STAMP(22);
   cluster_wait_acquire();  // no CTA leaves while another may still read its counts
