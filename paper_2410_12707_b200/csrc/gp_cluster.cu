@@ -211,22 +211,23 @@ __global__ void __launch_bounds__(kClThreads, 1) compress_cluster_kernel(const C
       for (uint32_t v = v0 + lane; v < v1; v += 32u) {
         const uint4 q4 = ld_shared_v4(xs + v * 16u);
         const uint32_t ne = v + 1u == nv ? nlast : (uint32_t)EPS;
+        uint32_t m = 0;  // keys of the bin: rare, handled below without per-element branches
 #pragma unroll
         for (int e = 0; e < EPS; ++e) {
+          const Key top = Tr::key(Tr::lane(q4, e)) >> hi;
+          const bool valid = (uint32_t)e < ne;
+          m |= (uint32_t)(valid && top == P) << e;
+          abv += (uint32_t)(valid && top > P);
+        }
+        while (m) {  // one list slot per key (a per-warp reservation measured 2x slower)
+          const int e = __ffs(m) - 1;
+          m &= m - 1;
           const Bits b = Tr::lane(q4, e);
-          const Key kk = Tr::key(b);
-          if ((uint32_t)e < ne) {
-            const Key top = kk >> hi;
-            if (top == P) {  // rare: one list slot per key (a per-warp reservation measured 2x slower)
-              atomicAdd(&h[(uint32_t)(kk >> lo) & mask], 1u);
-              const uint32_t j = atomicAdd(&res[8], 1u);
-              if (j < kListCap) {
-                lbits[j] = b;
-                lidx[j] = v * (uint32_t)EPS + (uint32_t)e;
-              }
-            } else if (top > P) {
-              ++abv;
-            }
+          atomicAdd(&h[(uint32_t)(Tr::key(b) >> lo) & mask], 1u);
+          const uint32_t j = atomicAdd(&res[8], 1u);
+          if (j < kListCap) {
+            lbits[j] = b;
+            lidx[j] = v * (uint32_t)EPS + (uint32_t)e;
           }
         }
       }
@@ -235,6 +236,13 @@ __global__ void __launch_bounds__(kClThreads, 1) compress_cluster_kernel(const C
     } else if (p >= 2 && list_ok) {
       const uint32_t nl = res[8];
       for (uint32_t j = tid; j < nl; j += kClThreads) add(lbits[j]);
+    } else if (p == 0) {  // every key matches the empty prefix: no test, no branch
+      for (uint32_t v = tid; v < nfull; v += kClThreads) {
+        const uint4 q4 = ld_shared_v4(xs + v * 16u);
+#pragma unroll
+        for (int e = 0; e < EPS; ++e) atomicAdd(&h[(uint32_t)(Tr::key(Tr::lane(q4, e)) >> lo) & mask], 1u);
+      }
+      if (tid < n - nfull * EPS) add(cl_elem_bits<Tr>(xe, nfull * EPS + tid));
     } else {
       for (uint32_t v = tid; v < nfull; v += kClThreads) {
         const uint4 q4 = ld_shared_v4(xs + v * 16u);
@@ -408,23 +416,24 @@ __global__ void __launch_bounds__(kClThreads, 1) compress_cluster_kernel(const C
 #pragma unroll
       for (int e = 0; e < EPS; ++e) {
         const Key kk = Tr::key(Tr::lane(q4, e));
-        if ((uint32_t)e < ne) {
-          gm |= (uint32_t)(kk > T) << e;
-          em |= (uint32_t)(kk == T) << e;
-        }
+        const bool valid = (uint32_t)e < ne;
+        gm |= (uint32_t)(valid && kk > T) << e;
+        em |= (uint32_t)(valid && kk == T) << e;
       }
     }
   };
   auto emit = [&](uint32_t v, const uint4& q4, uint32_t gm, uint32_t em, uint32_t g, uint32_t e2) {
     const uint32_t base = i0 + v * (uint32_t)EPS;
-#pragma unroll
-    for (int e = 0; e < EPS; ++e) {
+    uint32_t all = gm | em;  // in index order; a tie is kept while its rank is below q
+    while (all) {
+      const int e = __ffs(all) - 1;
+      all &= all - 1;
       if ((gm >> e) & 1u) {
         const uint32_t pos = g + min(q, e2);
         GP_CHECK(pos < k);
         cl_write_out<Tr>(a, val_out, pos, base + e, Tr::lane(q4, e));
         ++g;
-      } else if ((em >> e) & 1u) {
+      } else {
         if (e2 < q) {
           GP_CHECK(g + e2 < k);
           cl_write_out<Tr>(a, val_out, g + e2, base + e, Tr::lane(q4, e));
