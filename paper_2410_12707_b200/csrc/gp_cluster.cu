@@ -208,16 +208,33 @@ __global__ void __launch_bounds__(kClThreads, 1) compress_cluster_kernel(const C
       // warp counts its keys above the bin (all > T); later passes and the
       // count then read the list instead of the slice
       uint32_t abv = 0;
+      // the bin is [lo_in, hi_in) in key space; when both edges are finite
+      // non-zero keys each test is one |x| >= threshold compare (Tr::Cand, NaN
+      // false), else the integer key is computed (warp-uniform choice)
+      const Key lo_in = P << hi, hi_in = (P + 1) << hi;
+      const bool fast = lo_in >= 1 && hi_in - 1 <= Tr::kInfAbs;
+      const typename Tr::Cand c_lo = Tr::make_cand(fast ? lo_in - 1 : (Key)0);
+      const typename Tr::Cand c_hi = Tr::make_cand(fast ? hi_in - 1 : (Key)0);
       for (uint32_t v = v0 + lane; v < v1; v += 32u) {
         const uint4 q4 = ld_shared_v4(xs + v * 16u);
         const uint32_t ne = v + 1u == nv ? nlast : (uint32_t)EPS;
         uint32_t m = 0;  // keys of the bin: rare, handled below without per-element branches
+        if (fast) {
 #pragma unroll
-        for (int e = 0; e < EPS; ++e) {
-          const Key top = Tr::key(Tr::lane(q4, e)) >> hi;
-          const bool valid = (uint32_t)e < ne;
-          m |= (uint32_t)(valid && top == P) << e;
-          abv += (uint32_t)(valid && top > P);
+          for (int e = 0; e < EPS; ++e) {
+            const Bits b = Tr::lane(q4, e);
+            const bool valid = (uint32_t)e < ne, above = c_hi(b);
+            m |= (uint32_t)(valid && !above && c_lo(b)) << e;
+            abv += (uint32_t)(valid && above);
+          }
+        } else {
+#pragma unroll
+          for (int e = 0; e < EPS; ++e) {
+            const Key top = Tr::key(Tr::lane(q4, e)) >> hi;
+            const bool valid = (uint32_t)e < ne;
+            m |= (uint32_t)(valid && top == P) << e;
+            abv += (uint32_t)(valid && top > P);
+          }
         }
         while (m) {  // one list slot per key (a per-warp reservation measured 2x slower)
           const int e = __ffs(m) - 1;
@@ -406,6 +423,11 @@ __global__ void __launch_bounds__(kClThreads, 1) compress_cluster_kernel(const C
   // ---- write: kept (index, value) pairs in index order; two 32-vector steps
   // per iteration, so their load -> scan -> store chains overlap
   uint32_t gtb = res[4] + wcnt[w], eqb = res[5] + wcnt[32 + w];
+  // key > T as one |x| >= threshold compare and key == T as abs-bits == T - 1
+  // when T is a finite non-zero key (warp-uniform), else the integer key
+  const bool fastw = T >= 1 && T <= Tr::kInfAbs;
+  const typename Tr::Cand c_gt = Tr::make_cand(fastw ? T : (Key)0);
+  const Key tm1 = T - 1;
   auto masks = [&](uint32_t v, uint4& q4, uint32_t& gm, uint32_t& em) {
     gm = 0u;
     em = 0u;
@@ -413,12 +435,22 @@ __global__ void __launch_bounds__(kClThreads, 1) compress_cluster_kernel(const C
     if (v < v1) {
       q4 = ld_shared_v4(xs + v * 16u);
       const uint32_t ne = v + 1u == nv ? nlast : (uint32_t)EPS;
+      if (fastw) {
 #pragma unroll
-      for (int e = 0; e < EPS; ++e) {
-        const Key kk = Tr::key(Tr::lane(q4, e));
-        const bool valid = (uint32_t)e < ne;
-        gm |= (uint32_t)(valid && kk > T) << e;
-        em |= (uint32_t)(valid && kk == T) << e;
+        for (int e = 0; e < EPS; ++e) {
+          const Bits b = Tr::lane(q4, e);
+          const bool valid = (uint32_t)e < ne;
+          gm |= (uint32_t)(valid && c_gt(b)) << e;
+          em |= (uint32_t)(valid && Tr::abs_bits(b) == tm1) << e;
+        }
+      } else {
+#pragma unroll
+        for (int e = 0; e < EPS; ++e) {
+          const Key kk = Tr::key(Tr::lane(q4, e));
+          const bool valid = (uint32_t)e < ne;
+          gm |= (uint32_t)(valid && kk > T) << e;
+          em |= (uint32_t)(valid && kk == T) << e;
+        }
       }
     }
   };
