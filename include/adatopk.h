@@ -92,7 +92,7 @@ int gp_topk_compress_frame(const void* x, int dtype, int64_t d, int64_t k,
  * read into the CTAs' shared memory, DSMEM histograms, cluster barriers --
  * instead of the cooperative grid (identical results).  mode 1 (default): the
  * cluster kernel for vectors of at most 98,304 elements, where it is the
- * faster one on B200 (1.4-1.7x cold at 1K-64K elements); 2: for every vector that fits one
+ * faster one on B200 (1.4-1.9x cold at 1K-64K elements); 2: for every vector that fits one
  * 8-CTA cluster (up to 393,216 fp32 / 786,432 bf16 / 196,608 fp64 elements,
  * within max_ctas);
  * 0: never (also when the environment sets GP_NO_CLUSTER=1).  Returns the
